@@ -1,0 +1,18 @@
+"""B200-native AdaSpa hot path (arXiv 2502.21079).
+
+The four C-ABI entry points of include/adaspa.h, bound through ctypes:
+
+    dense_attn_lse     K1  dense attention forward + LSE           (Alg. 1 pass 1)
+    lse_cached_search  K2  block mass sum exp(S - LSE_cached)      (Alg. 2 / Alg. 1 pass 2)
+    select_blocks      K3  head-adaptive hierarchical selection -> CSR
+    block_sparse_attn  K4  block-sparse attention forward
+
+plus the host schedule (schedule.py) and head sharding / Ulysses exchange (dist.py).
+Importing fails loudly if libadaspa.so was not built: there is no CPU fallback.
+"""
+
+from ._lib import (  # noqa: F401
+    AttnDesc, AdaSpaError, Csr, abi_version, make_desc, num_blocks, dense_attn_lse, lse_cached_search,
+    select_blocks, block_sparse_attn, sparse_workspace_bytes, SELECT_RECALL, SELECT_SPARSITY,
+    FLAG_TEXT_SINK, FLAG_HEAD_TIERS, LIB_PATH,
+)

@@ -1,0 +1,402 @@
+// api.cu -- the C ABI of include/adaspa.h: argument validation, TMA tensor maps, workspace
+// layout and kernel launches.  No host synchronisation anywhere on this path.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+
+#include "../../include/adaspa.h"
+#include "attn.cuh"
+#include "common.cuh"
+#include "select.cuh"
+
+using namespace adaspa;
+
+namespace {
+
+thread_local std::string g_last_error = "no error";
+
+adaspa_status fail(adaspa_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+adaspa_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(ADASPA_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int num_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return 148;
+  return n;
+}
+
+BlockGrid make_grid(const adaspa_attn_desc* d) {
+  BlockGrid g;
+  g.n = d->seq_len;
+  g.bs = d->block_size;
+  const int n_video = d->seq_len - d->n_text;
+  g.n_first = d->text_first ? d->n_text : n_video;
+  g.nb_first = (g.n_first + g.bs - 1) / g.bs;
+  g.nb = g.nb_first + (d->seq_len - g.n_first + g.bs - 1) / g.bs;
+  return g;
+}
+
+adaspa_status check_desc(const adaspa_attn_desc* d) {
+  if (!d) return fail(ADASPA_ERR_INVALID_ARG, "desc is NULL");
+  if (d->batch < 1 || d->heads < 1 || d->seq_len < 1)
+    return fail(ADASPA_ERR_INVALID_ARG, "batch, heads and seq_len must be >= 1 (got %d, %d, %d)", d->batch,
+                d->heads, d->seq_len);
+  if (d->head_dim != 64 && d->head_dim != 128)
+    return fail(ADASPA_ERR_UNSUPPORTED, "head_dim %d unsupported (64 or 128)", d->head_dim);
+  if (d->block_size != 64 && d->block_size != 128)
+    return fail(ADASPA_ERR_UNSUPPORTED, "block_size %d unsupported (64 or 128)", d->block_size);
+  if (d->n_text < 0 || d->n_text > d->seq_len)
+    return fail(ADASPA_ERR_INVALID_ARG, "n_text %d outside [0, seq_len=%d]", d->n_text, d->seq_len);
+  if (d->text_first != 0 && d->text_first != 1) return fail(ADASPA_ERR_INVALID_ARG, "text_first must be 0 or 1");
+  if (!(d->softmax_scale == d->softmax_scale) || isinf(d->softmax_scale))
+    return fail(ADASPA_ERR_INVALID_ARG, "softmax_scale is not finite");
+  if (d->stride_n < 1 || d->stride_h < 1 || d->stride_b < 1)
+    return fail(ADASPA_ERR_INVALID_ARG, "strides must be >= 1");
+  if ((d->stride_n * 2) % 16 || (d->stride_h * 2) % 16 || (d->stride_b * 2) % 16)
+    return fail(ADASPA_ERR_INVALID_ARG, "strides must be multiples of 8 elements (16 bytes)");
+  if (d->stride_n < d->head_dim) return fail(ADASPA_ERR_INVALID_ARG, "stride_n < head_dim: rows overlap");
+  return ADASPA_OK;
+}
+
+float scale_of(const adaspa_attn_desc* d) {
+  return d->softmax_scale > 0.0f ? d->softmax_scale : 1.0f / sqrtf(static_cast<float>(d->head_dim));
+}
+
+adaspa_status check_ptr16(const void* p, const char* name) {
+  if (!p) return fail(ADASPA_ERR_INVALID_ARG, "%s is NULL", name);
+  if (reinterpret_cast<uintptr_t>(p) % 16) return fail(ADASPA_ERR_INVALID_ARG, "%s is not 16-byte aligned", name);
+  return ADASPA_OK;
+}
+
+adaspa_status make_map(CUtensorMap* map, const void* base, const adaspa_attn_desc* d, const char* name) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(ADASPA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  cuuint64_t dims[4] = {(cuuint64_t)d->head_dim, (cuuint64_t)d->seq_len, (cuuint64_t)d->heads,
+                        (cuuint64_t)d->batch};
+  cuuint64_t strides[3] = {(cuuint64_t)d->stride_n * 2, (cuuint64_t)d->stride_h * 2, (cuuint64_t)d->stride_b * 2};
+  cuuint32_t box[4] = {64, 64, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ADASPA_ERR_INVALID_ARG, "cuTensorMapEncodeTiled(%s) failed: %d", name, (int)r);
+  return ADASPA_OK;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct SelectWs {
+  size_t bits, nnz, kept, total, kbh, bytes;
+};
+SelectWs select_ws_layout(const adaspa_attn_desc* d) {
+  const BlockGrid g = make_grid(d);
+  const size_t rows = (size_t)d->batch * d->heads * g.nb;
+  const size_t nwords = (g.nb + 31) / 32;
+  SelectWs w;
+  size_t off = 0;
+  w.bits = off; off = align256(off + rows * nwords * 4);
+  w.nnz = off; off = align256(off + rows * 4);
+  w.kept = off; off = align256(off + rows * 8);
+  w.total = off; off = align256(off + rows * 8);
+  w.kbh = off; off = align256(off + (size_t)d->batch * d->heads * 4);
+  w.bytes = off;
+  return w;
+}
+
+struct SparseWs {
+  int items_per_bh, num_items, stride;
+  size_t queue, len, order, stream, bytes;
+};
+SparseWs sparse_ws_layout(const adaspa_attn_desc* d) {
+  const BlockGrid g = make_grid(d);
+  const bool two = d->block_size == 64;
+  SparseWs w;
+  w.items_per_bh = two ? (g.nb + 3) / 4 : (g.nb + 1) / 2;
+  w.num_items = d->batch * d->heads * w.items_per_bh;
+  w.stride = two ? (g.nb + 1) / 2 : g.nb;
+  size_t off = 0;
+  w.queue = off; off = align256(off + 4);
+  w.len = off; off = align256(off + (size_t)w.num_items * 4);
+  w.order = off; off = align256(off + (size_t)w.num_items * 4);
+  w.stream = off; off = align256(off + (size_t)w.num_items * w.stride * 4);
+  w.bytes = off;
+  return w;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t adaspa_abi_version(void) { return ADASPA_ABI_VERSION; }
+
+int32_t adaspa_num_blocks(const adaspa_attn_desc* desc) {
+  if (check_desc(desc) != ADASPA_OK) return -1;
+  return make_grid(desc).nb;
+}
+
+const char* adaspa_status_string(adaspa_status s) {
+  switch (s) {
+    case ADASPA_OK: return "ADASPA_OK";
+    case ADASPA_ERR_INVALID_ARG: return "ADASPA_ERR_INVALID_ARG";
+    case ADASPA_ERR_UNSUPPORTED: return "ADASPA_ERR_UNSUPPORTED";
+    case ADASPA_ERR_CUDA: return "ADASPA_ERR_CUDA";
+    case ADASPA_ERR_WORKSPACE_TOO_SMALL: return "ADASPA_ERR_WORKSPACE_TOO_SMALL";
+  }
+  return "ADASPA_ERR_UNKNOWN";
+}
+
+const char* adaspa_last_error(void) { return g_last_error.c_str(); }
+
+adaspa_status adaspa_dense_attn_lse(const adaspa_attn_desc* desc, const void* q, const void* k, const void* v,
+                                    void* o, float* lse, adaspa_stream_t stream) {
+  adaspa_status s;
+  if ((s = check_desc(desc)) != ADASPA_OK) return s;
+  if ((s = check_ptr16(q, "q")) || (s = check_ptr16(k, "k")) || (s = check_ptr16(v, "v")) ||
+      (s = check_ptr16(o, "o")))
+    return s;
+  CUtensorMap tq, tk, tv;
+  if ((s = make_map(&tq, q, desc, "q")) || (s = make_map(&tk, k, desc, "k")) || (s = make_map(&tv, v, desc, "v")))
+    return s;
+  AttnParams p{};
+  p.B = desc->batch;
+  p.H = desc->heads;
+  p.N = desc->seq_len;
+  p.grid = make_grid(desc);
+  p.scale_log2 = scale_of(desc) * kLog2e;
+  p.o = static_cast<__nv_bfloat16*>(o);
+  p.sb = desc->stride_b;
+  p.sh = desc->stride_h;
+  p.sn = desc->stride_n;
+  p.lse = lse;
+  p.items_per_bh = (desc->seq_len + 255) / 256;
+  p.num_items = desc->batch * desc->heads * p.items_per_bh;
+  cudaError_t e = launch_attn(tq, tk, tv, p, desc->head_dim, false, false, num_sms(), (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "dense_attn_lse launch");
+  return ADASPA_OK;
+}
+
+adaspa_status adaspa_lse_cached_search(const adaspa_attn_desc* desc, const void* q, const void* k,
+                                       const float* lse, float* block_mass, adaspa_stream_t stream) {
+  adaspa_status s;
+  if ((s = check_desc(desc)) != ADASPA_OK) return s;
+  if ((s = check_ptr16(q, "q")) || (s = check_ptr16(k, "k"))) return s;
+  if (!lse || !block_mass) return fail(ADASPA_ERR_INVALID_ARG, "lse and block_mass must not be NULL");
+  if (reinterpret_cast<uintptr_t>(lse) % 4 || reinterpret_cast<uintptr_t>(block_mass) % 4)
+    return fail(ADASPA_ERR_INVALID_ARG, "lse / block_mass misaligned");
+  CUtensorMap tq, tk;
+  if ((s = make_map(&tq, q, desc, "q")) || (s = make_map(&tk, k, desc, "k"))) return s;
+  SearchParams p{};
+  p.B = desc->batch;
+  p.H = desc->heads;
+  p.N = desc->seq_len;
+  p.grid = make_grid(desc);
+  p.scale_log2 = scale_of(desc) * kLog2e;
+  p.lse = lse;
+  p.mass = block_mass;
+  const bool two = desc->block_size == 64;
+  p.items_per_bh = two ? (p.grid.nb + 3) / 4 : (p.grid.nb + 1) / 2;
+  p.num_items = desc->batch * desc->heads * p.items_per_bh;
+  p.kv_tiles = two ? (p.grid.nb + 1) / 2 : p.grid.nb;
+  cudaError_t e = launch_search(tq, tk, p, desc->head_dim, two, num_sms(), (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "lse_cached_search launch");
+  return ADASPA_OK;
+}
+
+size_t adaspa_select_workspace_bytes(const adaspa_attn_desc* desc) {
+  if (check_desc(desc) != ADASPA_OK) return 0;
+  return select_ws_layout(desc).bytes;
+}
+
+adaspa_status adaspa_select_blocks(const adaspa_attn_desc* desc, const float* block_mass, adaspa_select_mode mode,
+                                   const double* target, uint32_t flags, double tier_tau, int32_t* row_ptr,
+                                   int32_t* col_idx, int64_t col_capacity, int32_t* row_order, float* head_recall,
+                                   int64_t* head_nnz, void* workspace, size_t workspace_bytes,
+                                   adaspa_stream_t stream) {
+  adaspa_status s;
+  if ((s = check_desc(desc)) != ADASPA_OK) return s;
+  if (!block_mass || !row_ptr || !col_idx || !target)
+    return fail(ADASPA_ERR_INVALID_ARG, "block_mass, target, row_ptr and col_idx must not be NULL");
+  if (mode != ADASPA_SELECT_RECALL && mode != ADASPA_SELECT_SPARSITY)
+    return fail(ADASPA_ERR_INVALID_ARG, "unknown selection mode %d", (int)mode);
+  if (flags & ~3u) return fail(ADASPA_ERR_INVALID_ARG, "unknown flag bits 0x%x", flags);
+  if (desc->heads > kMaxHeads) return fail(ADASPA_ERR_UNSUPPORTED, "heads > %d", kMaxHeads);
+  const BlockGrid g = make_grid(desc);
+  if (g.nb > 4096) return fail(ADASPA_ERR_UNSUPPORTED, "nb = %d > 4096 blocks", g.nb);
+  const int64_t rows = (int64_t)desc->batch * desc->heads * g.nb;
+  const int64_t need_cap = rows * g.nb;
+  if (need_cap > INT32_MAX) return fail(ADASPA_ERR_UNSUPPORTED, "B*H*nb*nb exceeds int32 CSR indexing");
+  if (col_capacity < need_cap)
+    return fail(ADASPA_ERR_INVALID_ARG, "col_capacity %lld < B*H*nb*nb = %lld", (long long)col_capacity,
+                (long long)need_cap);
+  const bool tiers = (flags & ADASPA_FLAG_HEAD_TIERS) != 0;
+  const bool sink = (flags & ADASPA_FLAG_TEXT_SINK) != 0;
+  if (tiers && mode != ADASPA_SELECT_SPARSITY)
+    return fail(ADASPA_ERR_INVALID_ARG, "ADASPA_FLAG_HEAD_TIERS applies to SPARSITY mode only");
+  for (int h = 0; h < desc->heads; ++h) {
+    const double t = target[h];
+    if (!(t == t) || isinf(t)) return fail(ADASPA_ERR_INVALID_ARG, "target[%d] is not finite", h);
+    if (mode == ADASPA_SELECT_SPARSITY && (t < 0.0 || t >= 1.0))
+      return fail(ADASPA_ERR_INVALID_ARG, "sparsity target[%d] = %g outside [0,1)", h, t);
+    if (tiers && t < 1.0 / 3.0)
+      return fail(ADASPA_ERR_INVALID_ARG, "head tiers need sparsity >= 1/3 (target[%d] = %g)", h, t);
+  }
+  if (tiers && !(tier_tau == tier_tau)) return fail(ADASPA_ERR_INVALID_ARG, "tier_tau is NaN");
+  const SelectWs w = select_ws_layout(desc);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ADASPA_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", workspace_bytes, w.bytes);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+
+  const int n_text_blocks = desc->text_first ? g.nb_first : g.nb - g.nb_first;
+  const int ncand = sink ? g.nb - n_text_blocks : g.nb;
+
+  SelectLaunch L{};
+  L.batch = desc->batch;
+  L.tiers = tiers;
+  SelectRowsParams& rp = L.rows;
+  rp.mass = block_mass;
+  rp.rows = static_cast<int>(rows);
+  rp.heads = desc->heads;
+  rp.grid = g;
+  rp.text_first = desc->text_first;
+  rp.text_sink = sink ? 1 : 0;
+  rp.mode = mode == ADASPA_SELECT_RECALL ? 0 : 1;
+  for (int h = 0; h < desc->heads; ++h) {
+    rp.target[h] = target[h];
+    rp.k_head[h] = mode == ADASPA_SELECT_SPARSITY ? k_from_sparsity(target[h], ncand) : 0;
+  }
+  rp.k_per_bh = nullptr;
+  rp.nwords = (g.nb + 31) / 32;
+  rp.bits = reinterpret_cast<uint32_t*>(ws + w.bits);
+  rp.row_nnz = reinterpret_cast<int*>(ws + w.nnz);
+  rp.row_kept = reinterpret_cast<double*>(ws + w.kept);
+  rp.row_total = reinterpret_cast<double*>(ws + w.total);
+  SelectTierParams& tp = L.tier;
+  tp.heads = desc->heads;
+  tp.nb = g.nb;
+  tp.ncand = ncand;
+  tp.tau = tier_tau;
+  for (int h = 0; h < desc->heads; ++h) tp.s_base[h] = target[h];
+  tp.row_kept = rp.row_kept;
+  tp.row_total = rp.row_total;
+  tp.k_per_bh = reinterpret_cast<int*>(ws + w.kbh);
+  SelectFinalParams& fp = L.fin;
+  fp.rows = rp.rows;
+  fp.nb = g.nb;
+  fp.bh = desc->batch * desc->heads;
+  fp.row_nnz = rp.row_nnz;
+  fp.row_kept = rp.row_kept;
+  fp.row_total = rp.row_total;
+  fp.row_ptr = row_ptr;
+  fp.row_order = row_order;
+  fp.head_recall = head_recall;
+  fp.head_nnz = head_nnz;
+  SelectWriteParams& wp = L.wr;
+  wp.rows = rp.rows;
+  wp.nwords = rp.nwords;
+  wp.bits = rp.bits;
+  wp.row_ptr = row_ptr;
+  wp.col_idx = col_idx;
+  cudaError_t e = launch_select(L, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "select_blocks launch");
+  return ADASPA_OK;
+}
+
+size_t adaspa_sparse_workspace_bytes(const adaspa_attn_desc* desc) {
+  if (check_desc(desc) != ADASPA_OK) return 0;
+  return sparse_ws_layout(desc).bytes;
+}
+
+adaspa_status adaspa_block_sparse_attn(const adaspa_attn_desc* desc, const void* q, const void* k, const void* v,
+                                       const int32_t* row_ptr, const int32_t* col_idx, void* o, float* lse,
+                                       void* workspace, size_t workspace_bytes, adaspa_stream_t stream) {
+  adaspa_status s;
+  if ((s = check_desc(desc)) != ADASPA_OK) return s;
+  if ((s = check_ptr16(q, "q")) || (s = check_ptr16(k, "k")) || (s = check_ptr16(v, "v")) ||
+      (s = check_ptr16(o, "o")))
+    return s;
+  if (!row_ptr || !col_idx) return fail(ADASPA_ERR_INVALID_ARG, "row_ptr / col_idx must not be NULL");
+  const BlockGrid g = make_grid(desc);
+  if (g.nb > 4095) return fail(ADASPA_ERR_UNSUPPORTED, "nb = %d > 4095 blocks", g.nb);
+  const SparseWs w = sparse_ws_layout(desc);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ADASPA_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", workspace_bytes, w.bytes);
+  CUtensorMap tq, tk, tv;
+  if ((s = make_map(&tq, q, desc, "q")) || (s = make_map(&tk, k, desc, "k")) || (s = make_map(&tv, v, desc, "v")))
+    return s;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const bool two = desc->block_size == 64;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(ws + w.queue, 0, 4, st);
+  if (e != cudaSuccess) return cuda_fail(e, "block_sparse_attn memset");
+  SparsePrepParams pp{};
+  pp.B = desc->batch;
+  pp.H = desc->heads;
+  pp.grid = g;
+  pp.two = two ? 1 : 0;
+  pp.items_per_bh = w.items_per_bh;
+  pp.num_items = w.num_items;
+  pp.row_ptr = row_ptr;
+  pp.col_idx = col_idx;
+  pp.stream = reinterpret_cast<uint32_t*>(ws + w.stream);
+  pp.stream_len = reinterpret_cast<int*>(ws + w.len);
+  pp.item_order = reinterpret_cast<int*>(ws + w.order);
+  pp.stream_stride = w.stride;
+  if ((e = launch_sparse_prep(pp, st)) != cudaSuccess) return cuda_fail(e, "block_sparse_attn prep");
+  AttnParams p{};
+  p.B = desc->batch;
+  p.H = desc->heads;
+  p.N = desc->seq_len;
+  p.grid = g;
+  p.scale_log2 = scale_of(desc) * kLog2e;
+  p.o = static_cast<__nv_bfloat16*>(o);
+  p.sb = desc->stride_b;
+  p.sh = desc->stride_h;
+  p.sn = desc->stride_n;
+  p.lse = lse;
+  p.items_per_bh = w.items_per_bh;
+  p.num_items = w.num_items;
+  p.item_order = pp.item_order;
+  p.stream = pp.stream;
+  p.stream_len = pp.stream_len;
+  p.stream_stride = w.stride;
+  p.queue = reinterpret_cast<int*>(ws + w.queue);
+  e = launch_attn(tq, tk, tv, p, desc->head_dim, two, true, num_sms(), st);
+  if (e != cudaSuccess) return cuda_fail(e, "block_sparse_attn launch");
+  return ADASPA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,64 @@
+// attn.cuh -- parameter blocks for the attention kernels (attn_fwd.cu: K1/K4, search.cu: K2).
+#pragma once
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace adaspa {
+
+// A stream entry of the block-sparse kernel: one 128-row kv tile made of one B=128 block
+// (id0) or two B=64 blocks (id0, id1), plus an 8-bit membership mask.  Mask bit
+// (4*t + 2*hq + hf) says that the 64-row half hq of q-tile t needs kv half hf.
+__host__ __device__ __forceinline__ uint32_t stream_entry(int id0, int id1, uint32_t mask) {
+  return static_cast<uint32_t>(id0) | (static_cast<uint32_t>(id1) << 12) | (mask << 24);
+}
+
+struct AttnParams {
+  int B, H, N;
+  BlockGrid grid;
+  float scale_log2;          // softmax_scale * log2(e)
+  __nv_bfloat16* o;          // output, same strides as Q/K/V
+  int64_t sb, sh, sn;        // element strides
+  float* lse;                // [B,H,N] or null
+  int num_items;             // work items (pairs of 128-row q tiles)
+  int items_per_bh;
+  // block-sparse only
+  const int* item_order;     // [num_items]: processing order (head-major, longest first in a head)
+  const uint32_t* stream;    // [num_items, stream_stride]
+  const int* stream_len;     // [num_items]
+  int stream_stride;
+  int* queue;                // atomic work counter
+};
+
+struct SparsePrepParams {
+  int B, H;
+  BlockGrid grid;
+  int two;                   // block 64 (two blocks per 128-row tile)
+  int items_per_bh, num_items;
+  const int32_t* row_ptr;
+  const int32_t* col_idx;
+  uint32_t* stream;
+  int* stream_len;
+  int* item_order;
+  int stream_stride;
+};
+
+struct SearchParams {
+  int B, H, N;
+  BlockGrid grid;
+  float scale_log2;
+  const float* lse;          // [B,H,N]
+  float* mass;               // [B,H,nb,nb]
+  int num_items;
+  int items_per_bh;
+  int kv_tiles;              // kv tiles per head
+};
+
+cudaError_t launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                        const AttnParams& p, int head_dim, bool two, bool sparse, int num_sms,
+                        cudaStream_t st);
+cudaError_t launch_sparse_prep(const SparsePrepParams& p, cudaStream_t st);
+cudaError_t launch_search(const CUtensorMap& tq, const CUtensorMap& tk, const SearchParams& p, int head_dim,
+                          bool two, int num_sms, cudaStream_t st);
+
+}  // namespace adaspa

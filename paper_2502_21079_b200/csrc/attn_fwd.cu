@@ -1,0 +1,690 @@
+// attn_fwd.cu -- K1 (dense attention + LSE) and K4 (head-adaptive block-sparse attention)
+// on sm_100a: TMA-staged Q/K/V tiles, tcgen05.mma into TMEM, softmax in registers.
+//
+// PAPER.md:194-202 (blockwise online softmax), 471-482 (Alg. 1 first pass: FA + LSE),
+// 415-427 (blockified sparse attention, -c(1-M) with c = +inf), 446-448 (visit only S*),
+// readings R1-R3 of DESIGN.md (garbled Alg. 1 initialisation / missing rescale / missing
+// normalisation -> the standard recurrence).
+//
+// Design (one CTA per SM, persistent):
+//   work item   = two 128-row q tiles (t = 0, 1) of one (b, h); dense: rows [256p, 256p+256);
+//                 sparse B=128: q-blocks 2p, 2p+1; sparse B=64: q-blocks 4p..4p+3.
+//   kv stream   = dense: every 128-row kv tile; sparse: the UNION of the tiles' CSR rows, each
+//                 entry tagged with which (q-tile, 64-row half) x (kv half) pairs need it, so
+//                 each K/V tile is loaded once for both q tiles.
+//   warp 0      TMA producer: Q tiles, then K,V tiles into a ring of NS slots.
+//   warp 1      MMA issuer (one thread): S_t = Q_t K^T (SS, M=128 N=128), O_t += P_t V
+//               (TS: P read from TMEM, V MN-major from smem, M=128 N=d).  Order per entry:
+//               PV_0(prev), QK_0(e), PV_1(prev), QK_1(e) -- softmax of one tile overlaps the
+//               MMAs of the other (ping-pong).
+//   warp 2      TMEM allocator (512 columns: S_0 | S_1 | O_0 | O_1).
+//   warps 4-7   softmax for q tile 0, warps 8-11 for q tile 1; thread = one row (TMEM lane).
+//               exp2 domain, conditional rescaling of O (only when the running max grows by
+//               more than 8 in log2 units -- exact, the final normalisation uses the same max),
+//               P written back to TMEM as bf16 over the first 64 columns of S_t.
+#include "attn.cuh"
+#include "common.cuh"
+
+namespace adaspa {
+
+namespace {
+
+constexpr int kThreads = 384;
+__device__ __forceinline__ uint32_t s_col(int t) { return static_cast<uint32_t>(t) * 128u; }
+__device__ __forceinline__ uint32_t o_col(int t) { return 256u + static_cast<uint32_t>(t) * 128u; }
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+enum : int { kNormal = 0, kEnd = 1, kAllEnd = 2 };
+
+struct SlotMeta {
+  int kind, mask, len0, len1;
+};
+
+struct TileInfo {
+  int kind;
+  int lim[4];      // [hq*2 + 0] column limit of kv half 0, [hq*2+1] of half 1 (exclusive, in 0..128)
+  int has;         // END: this tile had >= 1 entry in the item (O must be stored)
+  int b, h;
+  int start0, len0, start1, len1;
+};
+
+struct ItemInfo {
+  int b, h;
+  int exists[2];
+  int start0[2], len0[2], start1[2], len1[2];
+};
+
+template <int D>
+struct Smem {
+  static constexpr int kTile = 128 * D * 2;  // one 128-row tile of d bf16 columns
+  static constexpr int kNS = (D == 128) ? 5 : 10;
+  static constexpr int kQ = 0;
+  static constexpr int kKV = 2 * kTile;
+  static constexpr int kBar = kKV + kNS * kTile;
+  static constexpr int kBytes = kBar + 1024 + 1024;  // barriers/meta + alignment slack
+};
+
+struct Bars {
+  uint64_t kv_full[10], kv_empty[10];
+  uint64_t q_full, q_empty;
+  uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
+  SlotMeta meta[10];
+  TileInfo info[2][2];
+  ItemInfo qitem;
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void decode_item(const AttnParams& p, bool sparse, bool two, int id, ItemInfo& it) {
+  const int bh = id / p.items_per_bh;
+  const int pi = id - bh * p.items_per_bh;
+  it.b = bh / p.H;
+  it.h = bh - it.b * p.H;
+  if (!sparse) {
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int s = 256 * pi + 128 * t;
+      int l = p.N - s;
+      l = l < 0 ? 0 : (l > 128 ? 128 : l);
+      it.exists[t] = l > 0;
+      it.start0[t] = s;
+      it.len0[t] = l;
+      it.start1[t] = s + 64;
+      it.len1[t] = 0;
+    }
+  } else if (!two) {
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int qb = 2 * pi + t;
+      const bool ex = qb < p.grid.nb;
+      it.exists[t] = ex;
+      it.start0[t] = ex ? p.grid.start(qb) : 0;
+      it.len0[t] = ex ? p.grid.len(qb) : 0;
+      it.start1[t] = it.start0[t] + 64;
+      it.len1[t] = 0;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int qa = 4 * pi + 2 * t, qc = qa + 1;
+      const bool ea = qa < p.grid.nb, ec = qc < p.grid.nb;
+      it.exists[t] = ea;
+      it.start0[t] = ea ? p.grid.start(qa) : 0;
+      it.len0[t] = ea ? p.grid.len(qa) : 0;
+      it.start1[t] = ec ? p.grid.start(qc) : it.start0[t];
+      it.len1[t] = ec ? p.grid.len(qc) : 0;
+    }
+  }
+}
+
+template <int D, bool TWO, bool SPARSE>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                    const __grid_constant__ CUtensorMap tv, const AttnParams p) {
+  using S = Smem<D>;
+  constexpr int NS = S::kNS;
+  constexpr int TILE = S::kTile;
+  constexpr int CH = D / 64;            // 64-column (128-byte) chunks per row
+  constexpr int CHUNK = 128 * 128;      // bytes per chunk of a 128-row tile
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + S::kQ;
+  uint8_t* sKV = smem + S::kKV;
+  Bars* bars = reinterpret_cast<Bars*>(smem + S::kBar);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&bars->kv_full[i], 1);
+      mbar_init(&bars->kv_empty[i], 1);
+    }
+    mbar_init(&bars->q_full, 1);
+    mbar_init(&bars->q_empty, 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&bars->s_full[t], 2);
+      mbar_init(&bars->p_full[t], 4);
+      mbar_init(&bars->o_full[t], 1);
+      mbar_init(&bars->o_empty[t], 4);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tq);
+    tma_prefetch_desc(&tk);
+    tma_prefetch_desc(&tv);
+  }
+  if (warp == 2) {
+    tmem_alloc(&bars->tmem_base, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == 0) {
+    // ============================================================ TMA producer
+    if (lane == 0) {
+      int slot = 0;
+      uint32_t ph = 0, qph = 0;
+      const uint64_t pol_kv = l2_policy_evict_last();
+      const uint64_t pol_q = l2_policy_evict_first();
+      for (int it_n = 0;; ++it_n) {
+        int item;
+        if (SPARSE) item = atomicAdd(p.queue, 1);
+        else item = blockIdx.x + it_n * gridDim.x;
+        if (item >= p.num_items) break;
+        const int id = SPARSE ? __ldg(p.item_order + item) : item;
+        ItemInfo it;
+        decode_item(p, SPARSE, TWO, id, it);
+        mbar_wait(&bars->q_empty, qph ^ 1);
+        qph ^= 1;
+        bars->qitem = it;
+        const uint32_t qbytes = (it.exists[0] ? TILE : 0) + (it.exists[1] ? TILE : 0);
+        mbar_arrive_expect_tx(&bars->q_full, qbytes);
+        for (int t = 0; t < 2; ++t) {
+          if (!it.exists[t]) continue;
+          const int r1 = TWO ? it.start1[t] : it.start0[t] + 64;
+          for (int c = 0; c < CH; ++c) {
+            uint8_t* dst = sQ + t * TILE + c * CHUNK;
+            tma_load_4d_hint(&tq, &bars->q_full, dst, c * 64, it.start0[t], it.h, it.b, pol_q);
+            tma_load_4d_hint(&tq, &bars->q_full, dst + CHUNK / 2, c * 64, r1, it.h, it.b, pol_q);
+          }
+        }
+        const int n_ent = SPARSE ? __ldg(p.stream_len + id) : (p.N + 127) / 128;
+        const uint32_t* ent_ptr = SPARSE ? p.stream + static_cast<int64_t>(id) * p.stream_stride : nullptr;
+        const uint32_t dense_mask = (it.exists[0] ? 0x0Fu : 0u) | (it.exists[1] ? 0xF0u : 0u);
+        for (int e = 0; e < n_ent; ++e) {
+          int s0, l0, s1, l1;
+          uint32_t mask;
+          if (SPARSE) {
+            const uint32_t ent = __ldg(ent_ptr + e);
+            const int id0 = ent & 0xFFF, id1 = (ent >> 12) & 0xFFF;
+            mask = ent >> 24;
+            s0 = p.grid.start(id0);
+            l0 = p.grid.len(id0);
+            if (TWO) {
+              s1 = p.grid.start(id1);
+              l1 = p.grid.len(id1);
+            } else {
+              s1 = s0 + 64;
+              l1 = 0;
+            }
+          } else {
+            s0 = 128 * e;
+            l0 = p.N - s0 < 128 ? p.N - s0 : 128;
+            s1 = s0 + 64;
+            l1 = 0;
+            mask = dense_mask;
+          }
+          // K
+          mbar_wait(&bars->kv_empty[slot], ph ^ 1);
+          bars->meta[slot] = SlotMeta{kNormal, static_cast<int>(mask), l0, l1};
+          mbar_arrive_expect_tx(&bars->kv_full[slot], TILE);
+          for (int c = 0; c < CH; ++c) {
+            uint8_t* dst = sKV + slot * TILE + c * CHUNK;
+            tma_load_4d_hint(&tk, &bars->kv_full[slot], dst, c * 64, s0, it.h, it.b, pol_kv);
+            tma_load_4d_hint(&tk, &bars->kv_full[slot], dst + CHUNK / 2, c * 64, s1, it.h, it.b, pol_kv);
+          }
+          if (++slot == NS) { slot = 0; ph ^= 1; }
+          // V
+          mbar_wait(&bars->kv_empty[slot], ph ^ 1);
+          mbar_arrive_expect_tx(&bars->kv_full[slot], TILE);
+          for (int c = 0; c < CH; ++c) {
+            uint8_t* dst = sKV + slot * TILE + c * CHUNK;
+            tma_load_4d_hint(&tv, &bars->kv_full[slot], dst, c * 64, s0, it.h, it.b, pol_kv);
+            tma_load_4d_hint(&tv, &bars->kv_full[slot], dst + CHUNK / 2, c * 64, s1, it.h, it.b, pol_kv);
+          }
+          if (++slot == NS) { slot = 0; ph ^= 1; }
+        }
+        mbar_wait(&bars->kv_empty[slot], ph ^ 1);
+        bars->meta[slot].kind = kEnd;
+        mbar_arrive(&bars->kv_full[slot]);
+        if (++slot == NS) { slot = 0; ph ^= 1; }
+      }
+      mbar_wait(&bars->kv_empty[slot], ph ^ 1);
+      bars->meta[slot].kind = kAllEnd;
+      mbar_arrive(&bars->kv_full[slot]);
+    }
+  } else if (warp == 1) {
+    // ============================================================ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t kIdescQK = idesc_bf16(128, 128, false, false);
+      constexpr uint32_t kIdescPV = idesc_bf16(128, D, false, true);
+      const uint32_t sq_addr = smem_u32(sQ);
+      const uint32_t skv_addr = smem_u32(sKV);
+      int slot = 0;
+      uint32_t ph = 0, qph = 0;
+      uint32_t pph[2] = {0u, 0u}, oeph[2] = {0u, 0u};
+      int icnt[2] = {0, 0};
+      bool o_dirty[2] = {false, false};
+
+      auto issue_qk = [&](int t, int kslot) {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * CHUNK + (kk & 3) * 32;
+          const uint64_t a = desc_sw128(sq_addr + t * TILE + off, 16, 1024);
+          const uint64_t b = desc_sw128(skv_addr + kslot * TILE + off, 16, 1024);
+          mma_ss(tmem + s_col(t), a, b, kIdescQK, kk > 0 ? 1u : 0u);
+        }
+      };
+      auto issue_pv = [&](int t, int vslot, bool first) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t b = desc_sw128(skv_addr + vslot * TILE + kk * 2048, CHUNK, 1024);
+          mma_ts(tmem + o_col(t), tmem + s_col(t) + kk * 8, b, kIdescPV, (first && kk == 0) ? 0u : 1u);
+        }
+      };
+
+      for (;;) {
+        mbar_wait(&bars->kv_full[slot], ph);
+        tc_fence_after();
+        SlotMeta mt = bars->meta[slot];
+        if (mt.kind == kAllEnd) {
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            bars->info[t][icnt[t] & 1].kind = kAllEnd;
+            ++icnt[t];
+            mbar_arrive_n(&bars->s_full[t], 2);
+          }
+          break;
+        }
+        mbar_wait(&bars->q_full, qph);
+        qph ^= 1;
+        tc_fence_after();
+        const ItemInfo it = bars->qitem;
+        bool pend[2] = {false, false};
+        bool had[2] = {false, false};
+        bool first_pv[2] = {true, true};
+        int pvslot = -1;
+        uint32_t pvph = 0;
+        for (;;) {
+          if (mt.kind == kEnd) {
+            if (pvslot >= 0) {
+              mbar_wait(&bars->kv_full[pvslot], pvph);
+              tc_fence_after();
+            }
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              if (!pend[t]) continue;
+              mbar_wait(&bars->p_full[t], pph[t]);
+              pph[t] ^= 1;
+              tc_fence_after();
+              if (first_pv[t] && o_dirty[t]) {
+                mbar_wait(&bars->o_empty[t], oeph[t]);
+                oeph[t] ^= 1;
+                o_dirty[t] = false;
+                tc_fence_after();
+              }
+              issue_pv(t, pvslot, first_pv[t]);
+              first_pv[t] = false;
+            }
+            if (pvslot >= 0) tc_commit(&bars->kv_empty[pvslot]);
+            tc_commit(&bars->q_empty);
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              if (had[t]) {
+                tc_commit(&bars->o_full[t]);
+                o_dirty[t] = true;
+              }
+              TileInfo& inf = bars->info[t][icnt[t] & 1];
+              ++icnt[t];
+              inf.kind = kEnd;
+              inf.has = had[t];
+              inf.b = it.b;
+              inf.h = it.h;
+              inf.start0 = it.start0[t];
+              inf.len0 = it.len0[t];
+              inf.start1 = it.start1[t];
+              inf.len1 = it.len1[t];
+              mbar_arrive_n(&bars->s_full[t], 2);
+            }
+            mbar_arrive(&bars->kv_empty[slot]);
+            if (++slot == NS) { slot = 0; ph ^= 1; }
+            break;
+          }
+          // ---- normal entry: K in `slot`, V in the next slot
+          const int kslot = slot;
+          if (++slot == NS) { slot = 0; ph ^= 1; }
+          const int vslot = slot;
+          const uint32_t vph = ph;
+          if (++slot == NS) { slot = 0; ph ^= 1; }
+          if (pvslot >= 0) {
+            mbar_wait(&bars->kv_full[pvslot], pvph);
+            tc_fence_after();
+          }
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            if (pend[t]) {
+              mbar_wait(&bars->p_full[t], pph[t]);
+              pph[t] ^= 1;
+              tc_fence_after();
+              if (first_pv[t] && o_dirty[t]) {
+                mbar_wait(&bars->o_empty[t], oeph[t]);
+                oeph[t] ^= 1;
+                o_dirty[t] = false;
+                tc_fence_after();
+              }
+              issue_pv(t, pvslot, first_pv[t]);
+              first_pv[t] = false;
+              pend[t] = false;
+            }
+            const uint32_t need = (static_cast<uint32_t>(mt.mask) >> (4 * t)) & 0xFu;
+            if (need) {
+              issue_qk(t, kslot);
+              TileInfo& inf = bars->info[t][icnt[t] & 1];
+              ++icnt[t];
+              inf.kind = kNormal;
+#pragma unroll
+              for (int hq = 0; hq < 2; ++hq) {
+                const uint32_t bits = (need >> (2 * hq)) & 3u;
+                if (!TWO) {
+                  inf.lim[hq * 2 + 0] = (bits & 1u) ? (mt.len0 < 64 ? mt.len0 : 64) : 0;
+                  inf.lim[hq * 2 + 1] = (bits & 2u) ? mt.len0 : 64;
+                } else {
+                  inf.lim[hq * 2 + 0] = (bits & 1u) ? mt.len0 : 0;
+                  inf.lim[hq * 2 + 1] = (bits & 2u) ? 64 + mt.len1 : 64;
+                }
+              }
+              tc_commit(&bars->s_full[t]);
+              mbar_arrive(&bars->s_full[t]);
+              pend[t] = true;
+              had[t] = true;
+            }
+          }
+          if (pvslot >= 0) tc_commit(&bars->kv_empty[pvslot]);
+          tc_commit(&bars->kv_empty[kslot]);
+          pvslot = vslot;
+          pvph = vph;
+          mbar_wait(&bars->kv_full[slot], ph);
+          tc_fence_after();
+          mt = bars->meta[slot];
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ============================================================ softmax warps
+    const int t = (warp - 4) >> 2;
+    const int wq = warp & 3;                 // TMEM lane quarter
+    const int row = wq * 32 + lane;          // row of the q tile (TMEM lane)
+    const int hq = wq >> 1;                  // 64-row half
+    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+    const uint32_t s_addr = tmem + lane_base + s_col(t);
+    const uint32_t o_addr = tmem + lane_base + o_col(t);
+    const float sl2 = p.scale_log2;
+    uint32_t sph = 0, oph = 0;
+    int icnt = 0;
+    float m_used = -INFINITY, l_sum = 0.0f;
+    int ntile = 0;
+    for (;;) {
+      mbar_wait(&bars->s_full[t], sph);
+      sph ^= 1;
+      tc_fence_after();
+      const TileInfo& inf = bars->info[t][icnt & 1];
+      ++icnt;
+      const int kind = inf.kind;
+      if (kind == kAllEnd) break;
+      if (kind == kEnd) {
+        if (inf.has) {
+          const int b = inf.b, h = inf.h;
+          int tok;
+          bool valid;
+          if (!TWO) {
+            tok = inf.start0 + row;
+            valid = row < inf.len0;
+          } else if (row < 64) {
+            tok = inf.start0 + row;
+            valid = row < inf.len0;
+          } else {
+            tok = inf.start1 + row - 64;
+            valid = row - 64 < inf.len1;
+          }
+          mbar_wait(&bars->o_full[t], oph);
+          oph ^= 1;
+          tc_fence_after();
+          const float inv = l_sum > 0.0f ? 1.0f / l_sum : 0.0f;
+          __nv_bfloat16* optr = p.o + b * p.sb + h * p.sh + static_cast<int64_t>(tok) * p.sn;
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(o_addr + c * 32, r);
+            tmem_ld_wait32(r);
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]) * inv, __uint_as_float(r[2 * i + 1]) * inv);
+            if (valid) {
+              uint4* dst = reinterpret_cast<uint4*>(optr + c * 32);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            }
+          }
+          if (valid && p.lse) {
+            const float lv = l_sum > 0.0f ? (m_used + __log2f(l_sum)) * kLn2 : -INFINITY;
+            p.lse[(static_cast<int64_t>(b) * p.H + h) * p.N + tok] = lv;
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars->o_empty[t]);
+        }
+        m_used = -INFINITY;
+        l_sum = 0.0f;
+        ntile = 0;
+        continue;
+      }
+      const int lim0 = inf.lim[hq * 2 + 0];
+      const int lim1 = inf.lim[hq * 2 + 1];
+      const bool full = (lim0 == 64 && lim1 == 128);
+      // pass 1: row max over the valid columns (S read from TMEM in 32-column chunks)
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld32(s_addr + c * 32, r);
+        tmem_ld_wait32(r);
+        const int lim = c < 2 ? lim0 : lim1;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float v = __uint_as_float(r[i]);
+          mx = (full || c * 32 + i < lim) ? fmaxf(mx, v) : mx;
+        }
+      }
+      const float mx2 = mx * sl2;
+      const float m_new = fmaxf(m_used, mx2);
+      const bool grow = m_new > m_used + kRescaleThreshold;  // also true when m_used == -inf
+      float alpha = 1.0f;
+      if (grow) {
+        alpha = (m_used == -INFINITY) ? 0.0f : exp2f(m_used - m_new);
+        l_sum *= alpha;
+        m_used = m_new;
+      }
+      const bool rescale_o = grow && alpha != 0.0f && ntile > 0;
+      if (__any_sync(0xffffffffu, rescale_o)) {
+        const float a = rescale_o ? alpha : 1.0f;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(o_addr + c * 32, r);
+          tmem_ld_wait32(r);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * a);
+          tmem_st32(o_addr + c * 32, r);
+        }
+      }
+      const float mb = (m_used == -INFINITY) ? 0.0f : m_used;
+      // pass 2: P = 2^(S*scale*log2e - m), packed to bf16 pairs and written over the first 64
+      // columns of S_t (chunk c lands in columns [16c, 16c+16), already consumed).
+      float lsum = 0.0f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld32(s_addr + c * 32, r);
+        tmem_ld_wait32(r);
+        const int lim = c < 2 ? lim0 : lim1;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float p0 = ex2_approx(fmaf(__uint_as_float(r[2 * i]), sl2, -mb));
+          float p1 = ex2_approx(fmaf(__uint_as_float(r[2 * i + 1]), sl2, -mb));
+          if (!full) {
+            p0 = (c * 32 + 2 * i < lim) ? p0 : 0.0f;
+            p1 = (c * 32 + 2 * i + 1 < lim) ? p1 : 0.0f;
+          }
+          lsum += p0 + p1;
+          r[i] = pack_bf16x2(p0, p1);
+        }
+        tmem_st16(s_addr + c * 16, r);
+      }
+      l_sum += lsum;
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->p_full[t]);
+      ++ntile;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ sparse schedule prep
+// One warp per work item: union of the item's CSR rows (2 q-blocks at B=128, 4 at B=64) as a
+// bitmap pass over kv-block words, emitted in ascending order with membership masks.
+__global__ void __launch_bounds__(256) sparse_stream_kernel(SparsePrepParams p) {
+  const int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (item >= p.num_items) return;
+  const int bh = item / p.items_per_bh;
+  const int pi = item - bh * p.items_per_bh;
+  const int nb = p.grid.nb;
+  const int nq = p.two ? 4 : 2;
+  int rbeg[4], rend[4];
+  for (int s = 0; s < 4; ++s) {
+    const int qb = nq * pi + s;
+    if (s < nq && qb < nb) {
+      const int64_t row = static_cast<int64_t>(bh) * nb + qb;
+      rbeg[s] = p.row_ptr[row];
+      rend[s] = p.row_ptr[row + 1];
+    } else {
+      rbeg[s] = rend[s] = 0;
+    }
+  }
+  uint32_t* out = p.stream + static_cast<int64_t>(item) * p.stream_stride;
+  const int nwords = (nb + 31) / 32;
+  // cursors into each sorted list, advanced word by word (every lane walks all lists; lists are short)
+  int cur[4] = {rbeg[0], rbeg[1], rbeg[2], rbeg[3]};
+  int u_count = 0;  // union elements emitted so far
+  for (int w = 0; w < nwords; ++w) {
+    uint32_t word[4];
+    for (int s = 0; s < 4; ++s) {
+      uint32_t acc = 0;
+      // lane-parallel: each lane checks one candidate element of list s in this word
+      while (true) {
+        const int idx = cur[s] + lane;
+        int v = (idx < rend[s]) ? p.col_idx[idx] : 0x7fffffff;
+        const bool in = v < (w + 1) * 32;
+        if (in) acc |= 1u << (v - w * 32);
+        const uint32_t bal = __ballot_sync(0xffffffffu, in);
+        const int n_in = __popc(bal);
+        cur[s] += n_in;
+        if (n_in < 32) break;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc |= __shfl_xor_sync(0xffffffffu, acc, o);
+      word[s] = acc;
+    }
+    const uint32_t uni = word[0] | word[1] | word[2] | word[3];
+    const bool mine = (uni >> lane) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+    if (mine) {
+      const int pos = u_count + __popc(bal & ((1u << lane) - 1u));
+      const int j = w * 32 + lane;
+      uint32_t memb = 0;
+      for (int s = 0; s < 4; ++s) memb |= ((word[s] >> lane) & 1u) << s;
+      if (!p.two) {
+        const uint32_t mask = ((memb & 1u) ? 0x0Fu : 0u) | ((memb & 2u) ? 0xF0u : 0u);
+        out[pos] = stream_entry(j, j, mask);
+      } else {
+        const int hf = pos & 1;
+        uint32_t mask = 0;
+        for (int s = 0; s < 4; ++s)
+          if ((memb >> s) & 1u) mask |= 1u << (2 * s + hf);  // bit 4t + 2hq + hf with s = 2t + hq
+        const uint32_t part = (static_cast<uint32_t>(j) << (12 * hf)) | (mask << 24);
+        atomicOr(out + (pos >> 1), part);
+      }
+    }
+    u_count += __popc(bal);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    int n = u_count;
+    if (p.two) {
+      n = (u_count + 1) / 2;
+      if (u_count & 1) {  // odd union: duplicate id0 into the empty half (mask bits stay 0)
+        const uint32_t e = out[n - 1];
+        out[n - 1] = e | ((e & 0xFFFu) << 12);
+      }
+    }
+    p.stream_len[item] = n;
+  }
+}
+
+// One CTA per (b,h): order the head's items by stream length, longest first (LPT within a
+// head; heads stay in order so concurrently running CTAs share one head's K/V in L2).
+__global__ void __launch_bounds__(256) sparse_order_kernel(SparsePrepParams p) {
+  const int bh = blockIdx.x;
+  const int P = p.items_per_bh;
+  const int base = bh * P;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    const int ci = p.stream_len[base + i];
+    int rank = 0;
+    for (int j = 0; j < P; ++j) {
+      const int cj = p.stream_len[base + j];
+      rank += (cj > ci || (cj == ci && j < i)) ? 1 : 0;
+    }
+    p.item_order[base + rank] = base + i;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_sparse_prep(const SparsePrepParams& p, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(p.stream, 0, sizeof(uint32_t) * static_cast<size_t>(p.num_items) * p.stream_stride, st);
+  if (e != cudaSuccess) return e;
+  const int blocks = (p.num_items * 32 + 255) / 256;
+  sparse_stream_kernel<<<blocks, 256, 0, st>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  sparse_order_kernel<<<p.B * p.H, 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int D, bool TWO, bool SPARSE>
+static cudaError_t launch_one(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                              const AttnParams& p, int num_sms, cudaStream_t st) {
+  auto kern = attn_fwd_kernel<D, TWO, SPARSE>;
+  const int smem = Smem<D>::kBytes;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = p.num_items < num_sms ? p.num_items : num_sms;
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                        const AttnParams& p, int head_dim, bool two, bool sparse, int num_sms,
+                        cudaStream_t st) {
+  if (head_dim == 128) {
+    if (!sparse) return launch_one<128, false, false>(tq, tk, tv, p, num_sms, st);
+    return two ? launch_one<128, true, true>(tq, tk, tv, p, num_sms, st)
+               : launch_one<128, false, true>(tq, tk, tv, p, num_sms, st);
+  }
+  if (!sparse) return launch_one<64, false, false>(tq, tk, tv, p, num_sms, st);
+  return two ? launch_one<64, true, true>(tq, tk, tv, p, num_sms, st)
+             : launch_one<64, false, true>(tq, tk, tv, p, num_sms, st);
+}
+
+}  // namespace adaspa

@@ -1,0 +1,69 @@
+// select.cuh -- parameter blocks of the K3 selection kernels (select.cu).
+#pragma once
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace adaspa {
+
+constexpr int kMaxHeads = 256;
+
+struct SelectRowsParams {
+  const float* mass;      // [rows, nb]
+  int rows;               // B*H*nb
+  int heads;
+  BlockGrid grid;
+  int text_first;
+  int text_sink;
+  int mode;               // 0 recall, 1 sparsity
+  double target[kMaxHeads];  // recall targets (mode 0)
+  int k_head[kMaxHeads];     // sparsity budgets per head (mode 1, no tiers)
+  const int* k_per_bh;       // sparsity budgets per (b,h) (tiers pass 2) or null
+  int nwords;             // ceil(nb/32)
+  uint32_t* bits;         // [rows, nwords]
+  int* row_nnz;           // [rows]
+  double* row_kept;       // [rows]
+  double* row_total;      // [rows]
+};
+
+struct SelectTierParams {
+  int heads, nb, ncand;
+  double tau;
+  double s_base[kMaxHeads];
+  const double* row_kept;
+  const double* row_total;
+  int* k_per_bh;          // [B*H] output
+};
+
+struct SelectFinalParams {
+  int rows, nb, bh;
+  const int* row_nnz;
+  const double* row_kept;
+  const double* row_total;
+  int32_t* row_ptr;
+  int32_t* row_order;     // may be null
+  float* head_recall;     // may be null
+  int64_t* head_nnz;      // may be null
+};
+
+struct SelectWriteParams {
+  int rows, nwords;
+  const uint32_t* bits;
+  const int32_t* row_ptr;
+  int32_t* col_idx;
+};
+
+struct SelectLaunch {
+  int batch;
+  bool tiers;
+  SelectRowsParams rows;
+  SelectTierParams tier;
+  SelectFinalParams fin;
+  SelectWriteParams wr;
+};
+
+cudaError_t launch_select(const SelectLaunch& L, cudaStream_t st);
+
+__host__ __device__ int k_from_sparsity(double s, int n);
+
+}  // namespace adaspa

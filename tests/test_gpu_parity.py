@@ -1,0 +1,197 @@
+"""GPU parity of the four C-ABI calls against the fp64 oracle on seeded inputs
+(small sizes that still span several tiles plus ragged tails).  Run on a B200:
+    python -m pytest tests -m gpu -x -q
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+from gpu_helpers import (MASS_REL, O_MAX_ABS, compare_out, csr_rows, np64, selection_ok)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ada():
+    import paper_2502_21079_b200.build as b
+    b.build()
+    import paper_2502_21079_b200 as m
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    return m
+
+
+def _qkv(lay, seed=workloads.synth.BASE_SEED, heads=None, batch=1):
+    q, k, v = workloads.generate_qkv(lay, batch=batch, seed=seed, heads=heads)
+    return q.cuda(), k.cuda(), v.cuda()
+
+
+CASES = [
+    # name, overrides (layouts chosen to span several 128-row tiles with ragged tails)
+    ("tiny", {}),
+    ("tiny_tf", {}),
+    ("tiny", dict(f=5, h=9, w=11, n_text=37, head_dim=128, block=128)),      # 495 + 37 tokens, d=128
+    ("tiny_tf", dict(f=3, h=10, w=13, n_text=77, head_dim=64, block=128)),   # text first, B=128
+    ("tiny", dict(f=4, h=9, w=10, n_text=45, head_dim=128, block=64, heads=3)),
+]
+
+
+def _lay(name, over):
+    return workloads.layout_for(name, **over)
+
+
+@pytest.mark.parametrize("name,over", CASES)
+def test_dense_attn_lse(ada, name, over):
+    lay = _lay(name, over)
+    q, k, v = _qkv(lay)
+    o, lse = ada.dense_attn_lse(q, k, v, block_size=lay.block, n_text=lay.n_text, text_first=lay.text_first)
+    torch.cuda.synchronize()
+    scale = 1 / math.sqrt(lay.head_dim)
+    for h in range(lay.heads):
+        ro, rl = oracle.dense_attention(np64(q[0, h]), np64(k[0, h]), np64(v[0, h]), scale)
+        compare_out(o[0, h], ro, lse[0, h], rl, what=f"{name} h{h}")
+
+
+def test_dense_token_major_layout(ada):
+    """[B, N, H, d] storage (Ulysses layout) through the stride arguments."""
+    lay = _lay("tiny", dict(heads=3, head_dim=128, block=128))
+    q, k, v = _qkv(lay, batch=2)
+    qt, kt, vt = (x.transpose(1, 2).contiguous().transpose(1, 2) for x in (q, k, v))
+    assert qt.stride(2) == 3 * 128
+    o, lse = ada.dense_attn_lse(qt, kt, vt, block_size=128, n_text=lay.n_text)
+    o2, lse2 = ada.dense_attn_lse(q, k, v, block_size=128, n_text=lay.n_text)
+    torch.cuda.synchronize()
+    assert torch.equal(o, o2) and torch.equal(lse, lse2)
+    ro, rl = oracle.dense_attention(np64(q[1, 2]), np64(k[1, 2]), np64(v[1, 2]), 1 / math.sqrt(128))
+    compare_out(o[1, 2], ro, lse[1, 2], rl, what="token-major b1 h2")
+
+
+@pytest.mark.parametrize("name,over", CASES)
+def test_search_block_mass(ada, name, over):
+    """K2 with the oracle's exact LSE as the cached LSE: masses vs the explicit fp64 matrix,
+    and row sums = |q-block|."""
+    lay = _lay(name, over)
+    q, k, v = _qkv(lay)
+    scale = 1 / math.sqrt(lay.head_dim)
+    blocks = oracle.block_map(lay.n_video, lay.n_text, lay.block, lay.text_first)
+    lse_ref = []
+    for h in range(lay.heads):
+        _, rl = oracle.dense_attention(np64(q[0, h]), np64(k[0, h]), np64(v[0, h]), scale)
+        lse_ref.append(rl)
+    lse_t = torch.tensor(np.stack(lse_ref)[None], dtype=torch.float32, device="cuda")
+    M = ada.lse_cached_search(q, k, lse_t, block_size=lay.block, n_text=lay.n_text, text_first=lay.text_first)
+    torch.cuda.synchronize()
+    L = np.array([b.length for b in blocks], dtype=np.float64)
+    for h in range(lay.heads):
+        # the oracle takes the same fp32 LSE the kernel reads
+        Mo = oracle.block_mass(np64(q[0, h]), np64(k[0, h]), lse_t[0, h].double().cpu().numpy(), blocks, scale)
+        err = np.abs(M[0, h].double().cpu().numpy() - Mo) / L[:, None]
+        assert err.max() <= MASS_REL, f"{name} h{h}: max |dM|/|qb| = {err.max():.3e}"
+        rs = M[0, h].double().cpu().numpy().sum(axis=1) / L
+        assert np.abs(rs - Mo.sum(axis=1) / L).max() <= 1e-5
+
+
+@pytest.mark.parametrize("tf", [False, True])
+@pytest.mark.parametrize("mode", ["recall", "sparsity", "tiers", "nosink"])
+def test_select_blocks_exact(ada, tf, mode):
+    """K3 alone: identical fp32 masses on both sides -> identical CSR (bit-exact)."""
+    H, nv, nt, B = 6, 1000, 150, 64
+    blocks = oracle.block_map(nv, nt, B, tf)
+    nb = len(blocks)
+    Mt = workloads.random_masses(H * nb, nb, seed=7 + tf).view(1, H, nb, nb)
+    q = torch.empty(1, H, nv + nt, 64, dtype=torch.bfloat16, device="cuda")
+    desc = ada.make_desc(q, B, nt, tf)
+    sink = mode != "nosink"
+    if mode in ("recall", "nosink"):
+        targets = [0.5, 0.8, 0.9, 0.95, 0.99, 1.0]
+        kmode, flags = ada.SELECT_RECALL, (1 if sink else 0)
+    elif mode == "sparsity":
+        targets = [0.0, 0.5, 0.7, 0.8, 0.9, 0.95]
+        kmode, flags = ada.SELECT_SPARSITY, 1
+    else:
+        targets = [0.8] * H
+        kmode, flags = ada.SELECT_SPARSITY, 3
+    out = ada.select_blocks(Mt.cuda(), heads_desc=desc, mode=kmode, target=targets, flags=flags, tier_tau=0.8)
+    torch.cuda.synchronize()
+    M64 = Mt[0].double().numpy()
+    keep, rec, nnz, _ = oracle.select_blocks(M64, blocks, "recall" if kmode == 0 else "sparsity", targets,
+                                             text_sink=sink, tiers=(mode == "tiers"))
+    rows = csr_rows(out.row_ptr, out.col_idx)
+    for h in range(H):
+        for p in range(nb):
+            exp = np.nonzero(keep[h, p])[0].tolist()
+            assert rows[h * nb + p] == exp, f"h{h} row {p}: {rows[h * nb + p][:8]} vs {exp[:8]}"
+    np.testing.assert_array_equal(out.head_nnz[0].cpu().numpy(), nnz)
+    np.testing.assert_allclose(out.head_recall[0].cpu().numpy(), rec, rtol=1e-6)
+    order = out.row_order.cpu().numpy()
+    cnt = np.diff(out.row_ptr.cpu().numpy())
+    assert sorted(order.tolist()) == list(range(H * nb))
+    assert (np.diff(cnt[order]) <= 0).all()
+
+
+def _random_csr(H, nb, density, seed):
+    g = np.random.default_rng(seed)
+    keep = g.random((H, nb, nb)) < density
+    keep[:, np.arange(nb), g.integers(0, nb, nb)] = True
+    rp = [0]
+    ci = []
+    for r in keep.reshape(-1, nb):
+        ids = np.nonzero(r)[0].tolist()
+        ci += ids
+        rp.append(len(ci))
+    return keep, torch.tensor(rp, dtype=torch.int32, device="cuda"), torch.tensor(ci, dtype=torch.int32, device="cuda")
+
+
+@pytest.mark.parametrize("name,over", CASES)
+@pytest.mark.parametrize("density", [0.3, 1.0])
+def test_block_sparse_attn(ada, name, over, density):
+    """K4 vs oracle masked attention (c = +inf) on the same CSR."""
+    lay = _lay(name, over)
+    q, k, v = _qkv(lay)
+    blocks = oracle.block_map(lay.n_video, lay.n_text, lay.block, lay.text_first)
+    nb = len(blocks)
+    keep, rp, ci = _random_csr(lay.heads, nb, density, 11)
+    o, lse = ada.block_sparse_attn(q, k, v, rp, ci, block_size=lay.block, n_text=lay.n_text,
+                                   text_first=lay.text_first, want_lse=True)
+    torch.cuda.synchronize()
+    scale = 1 / math.sqrt(lay.head_dim)
+    for h in range(lay.heads):
+        kept = [np.nonzero(keep[h, p])[0] for p in range(nb)]
+        ro, rl = oracle.masked_attention(np64(q[0, h]), np64(k[0, h]), np64(v[0, h]), blocks, kept, scale)
+        # masked_attention returns rows in q-block order = token order
+        compare_out(o[0, h], ro, lse[0, h], rl, what=f"{name} d={density} h{h}")
+
+
+def test_end_to_end_tiny(ada):
+    """K1 -> K2 (fresh LSE) -> K3 (recall 0.9) -> K4 against the oracle pipeline, both text orders."""
+    for name in ("tiny", "tiny_tf"):
+        lay = workloads.layout_for(name)
+        q, k, v = _qkv(lay)
+        kw = dict(block_size=lay.block, n_text=lay.n_text, text_first=lay.text_first)
+        o_d, lse = ada.dense_attn_lse(q, k, v, **kw)
+        M = ada.lse_cached_search(q, k, lse, **kw)
+        desc = ada.make_desc(q, lay.block, lay.n_text, lay.text_first)
+        out = ada.select_blocks(M, heads_desc=desc, mode=ada.SELECT_RECALL, target=[0.9] * lay.heads)
+        o_s, _ = ada.block_sparse_attn(q, k, v, out.row_ptr, out.col_idx, **kw)
+        torch.cuda.synchronize()
+        blocks = oracle.block_map(lay.n_video, lay.n_text, lay.block, lay.text_first)
+        nb = len(blocks)
+        scale = 1 / math.sqrt(lay.head_dim)
+        rows = csr_rows(out.row_ptr, out.col_idx)
+        for h in range(lay.heads):
+            qq, kk, vv = np64(q[0, h]), np64(k[0, h]), np64(v[0, h])
+            ro, rl = oracle.dense_attention(qq, kk, vv, scale)
+            compare_out(o_d[0, h], ro, lse[0, h], rl, what=f"{name} dense h{h}")
+            Mo = oracle.block_mass(qq, kk, rl, blocks, scale)
+            for p in range(nb):
+                forced, cands = oracle.row_forced_and_candidates(blocks, p, True)
+                ok = oracle.select_row_recall(Mo[p], forced, cands, 0.9)
+                good, msg = selection_ok(Mo[p], forced, cands, 0.9, rows[h * nb + p], ok)
+                assert good, f"{name} h{h} row {p}: {msg}"
+            gk = [rows[h * nb + p] for p in range(nb)]
+            so, _ = oracle.masked_attention(qq, kk, vv, blocks, gk, scale)
+            compare_out(o_s[0, h], so, what=f"{name} sparse h{h}")
