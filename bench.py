@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""bench.py -- AdaSpa hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config hyv110k]
+
+A step is one pass of the whole hot path over one HunyuanVideo-shaped layer
+(BASELINE.json configs[2]: H=24, d=128, ~110K tokens, block 128, head-adaptive recall 0.9):
+K1 dense attention + LSE -> K2 LSE-cached block-mass search -> K3 selection -> K4 block-sparse
+forward.  metric = BASELINE.json's metric; `value` = effective TFLOP/s of the block-sparse forward
+on kept blocks (4*d*sum_kept |qb||kb| / K4 time), whole job: sum over ranks / max over ranks.
+ms/layer, the search overhead and every kernel's roofline are extra keys.
+
+Multi-GPU (torchrun): weak scaling -- every rank runs its own layer (its own seed) on its own GPU;
+the path has no exchange step, so there is no data-path collective.
+`--impl reference`: the fp64 oracle (oracle/) timed on the host cores on a bounded sample.
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+METRIC = "block-sparse attn effective TFLOP/s & ms/layer @110K tok; search overhead ms"
+UNIT = "TFLOP/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="hyv110k")
+    ap.add_argument("--recall", type=float, default=0.9)
+    ap.add_argument("--mode", default="recall", choices=["recall", "sparsity-tiers"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, \
+        "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.count(",") >= 6]
+        os.unlink(self.f.name)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], None, set()
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+            except ValueError:
+                continue
+            for i, n in enumerate(names):
+                if "Active" in r[3 + i] and "Not" not in r[3 + i]:
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def block_lengths(lay):
+    """Valid token count of each block of the modality-aware grid."""
+    B = lay.block
+    n_first = lay.n_text if lay.text_first else lay.n_video
+    out = []
+    for start, stop in ((0, n_first), (n_first, lay.n)):
+        for s in range(start, stop, B):
+            out.append(min(B, stop - s))
+    return out
+
+
+def kept_flops(lay, csr, d):
+    """4 * d * sum over kept (q-block, kv-block) pairs of |qb| * |kb| (partial blocks counted exactly)."""
+    L = torch.tensor(block_lengths(lay), dtype=torch.float64, device=csr.row_ptr.device)
+    nbk = L.numel()
+    rp = csr.row_ptr.long()
+    nnz = int(rp[-1].item())
+    rows = torch.repeat_interleave(torch.arange(rp.numel() - 1, device=rp.device), rp[1:] - rp[:-1])
+    ci = csr.col_idx[:nnz].long()
+    return 4.0 * d * float((L[rows % nbk] * L[ci]).sum().item()), nnz
+
+
+def roofline_entry(bound, achieved, peak, unit, traffic=None, **extra):
+    e = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
+         "frac": round(achieved / peak, 4) if peak else None, "traffic": traffic}
+    e.update(extra)
+    return e
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except ValueError:
+            return {}
+    return {}
+
+
+def cpu_baseline_sample(lay, q, k, v, csr, seconds):
+    """The oracle's block-sparse forward (masked attention) on head 0's q-blocks in
+    order, with the GPU's CSR, until `seconds` of CPU time: effective TFLOP/s on kept blocks."""
+    import numpy as np
+    import oracle
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:  # noqa: BLE001
+        cores = os.cpu_count()
+    blocks = oracle.block_map(lay.n_video, lay.n_text, lay.block, lay.text_first)
+    nb = len(blocks)
+    rp = csr.row_ptr[: nb + 1].cpu().numpy()
+    ci = csr.col_idx[: int(rp[-1])].cpu().numpy()
+    qh, kh, vh = (x[0, 0].float().double().cpu().numpy() for x in (q, k, v))
+    scale = 1.0 / math.sqrt(lay.head_dim)
+    t0 = time.perf_counter()
+    flops, done = 0.0, 0
+    order = list(range(0, nb, max(1, nb // 64)))
+    for p in order:
+        kept = {p: ci[rp[p]:rp[p + 1]].tolist()}
+        oracle.masked_attention(qh, kh, vh, blocks, kept, scale, q_block_ids=[p])
+        flops += 4.0 * lay.head_dim * blocks[p].length * sum(blocks[j].length for j in kept[p])
+        done += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(flops / dt / 1e12, 6), "unit": UNIT, "cores": int(cores), "kind": "oracle",
+            "sample": f"oracle masked attention (fp64 numpy) for {done} q-blocks of head 0 at {lay.name} "
+                      f"with the GPU's CSR ({dt:.1f} s)"}
+
+
+def run_ours(args):
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    import workloads
+    import paper_2502_21079_b200 as ada
+    from paper_2502_21079_b200.hotpath import HotPath
+
+    lay = workloads.layout_for(args.config)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    seed = workloads.synth.BASE_SEED + 101 * rank
+    q, k, v = workloads.generate_qkv(lay, device=dev, seed=seed)
+    if args.mode == "recall":
+        hp = HotPath(1, lay.heads, lay.n, lay.head_dim, lay.block, lay.n_text, lay.text_first,
+                     mode=ada.SELECT_RECALL, targets=args.recall, flags=ada.FLAG_TEXT_SINK)
+    else:
+        hp = HotPath(1, lay.heads, lay.n, lay.head_dim, lay.block, lay.n_text, lay.text_first,
+                     mode=ada.SELECT_SPARSITY, targets=0.8, flags=ada.FLAG_TEXT_SINK | ada.FLAG_HEAD_TIERS)
+    for _ in range(args.warmup):
+        hp.run(q, k, v)
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(dev.index)
+    t_wall = time.perf_counter()
+    for s in range(args.steps):
+        hp.run(q, k, v, events=ev[s])
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_wall
+    if ws > 1:
+        torch.distributed.barrier()
+    clocks = clk.stop()
+    per = [[ev[s][i].elapsed_time(ev[s][i + 1]) for i in range(4)] for s in range(args.steps)]
+    tk = [sum(p[i] for p in per) for i in range(4)]          # ms over K steps, per kernel
+    total = sum(tk)
+    kfl, nnz = kept_flops(lay, hp.csr, lay.head_dim)
+    nb = hp.nb
+    H, N, d = lay.heads, lay.n, lay.head_dim
+    t = torch.tensor([total, tk[3], tk[0], tk[1], tk[2]], dtype=torch.float64, device=dev)
+    work = torch.tensor([kfl], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(work, op=torch.distributed.ReduceOp.SUM)
+    total_max, k4_max = float(t[0]), float(t[1])
+    K = args.steps
+    value = work.item() * K / (k4_max / 1e3) / 1e12
+
+    # e2e: the same metric through the public API with host buffers (pinned), copies timed
+    e2e = None
+    if not args.no_e2e:
+        qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
+        oh = torch.empty_like(qh).pin_memory()
+        for _ in range(2):
+            hp.run(qh, kh, vh)
+            oh.copy_(hp.o_sparse, non_blocking=True)
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if ws > 1:
+            torch.distributed.barrier()
+        s0.record()
+        for _ in range(K):
+            hp.run(qh, kh, vh)
+            oh.copy_(hp.o_sparse, non_blocking=True)
+        s1.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([s0.elapsed_time(s1)], dtype=torch.float64, device=dev)
+        if ws > 1:
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": round(work.item() * K / (te.item() / 1e3) / 1e12, 3), "unit": UNIT,
+               "h2d_bytes_per_step": 3 * q.numel() * q.element_size(),
+               "d2h_bytes_per_step": q.numel() * q.element_size(),
+               "ms_per_step": round(te.item() / K, 3),
+               "note": "TFLOP/s on kept blocks over the whole step incl. H2D of Q,K,V and D2H of O (pinned)"}
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return
+    peaks, src = load_peaks()
+    tens_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    exp_peak = 16.0 * 148 * sm_max * 1e6 / 1e12      # MUFU.EX2 16/clk/SM (T exp/s)
+    traffic = load_traffic()
+    ms = [x / K for x in tk]
+    dense_fl = 4.0 * N * N * d * H
+    k3_bytes = 4.0 * nb * nb * H + 4.0 * (H * nb + 1) + 4.0 * nnz + 4.0 * H * nb
+    kern = {
+        "K1_dense_attn_lse": roofline_entry("tensor", dense_fl / (ms[0] / 1e3) / 1e12, tens_peak, "TFLOP/s",
+                                            traffic.get("K1"), ms=round(ms[0], 3)),
+        "K2_lse_cached_search": roofline_entry("alu", N * N * H / (ms[1] / 1e3) / 1e12, exp_peak, "Texp/s",
+                                               traffic.get("K2"), ms=round(ms[1], 3),
+                                               tensor_tflops=round(dense_fl / 2 / (ms[1] / 1e3) / 1e12, 1)),
+        "K3_select_blocks": roofline_entry("hbm", k3_bytes / (ms[2] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s",
+                                           traffic.get("K3"), ms=round(ms[2], 4)),
+        "K4_block_sparse_attn": roofline_entry("tensor", kfl / (ms[3] / 1e3) / 1e12, tens_peak, "TFLOP/s",
+                                               traffic.get("K4"), ms=round(ms[3], 3)),
+    }
+    dom = max(range(4), key=lambda i: ms[i])
+    dom_name = list(kern)[dom]
+    roof = dict(kern[dom_name])
+    roof["kernel"] = dom_name
+    roof["peak_source"] = f"{src} ({'bf16_tflops_sustained' if roof['bound'] == 'tensor' else 'see kernels'})"
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(lay, q, k, v, hp.csr, args.cpu_seconds)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
+        "ms_per_step": round(total_max / K, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (workloads/synth.py, seeded; DESIGN.md §5)",
+        "config": {"workload": lay.name, "seq_len": N, "heads": H, "head_dim": d, "block": lay.block,
+                   "n_text": lay.n_text, "selection": (f"recall {args.recall} per head, text sink"
+                                                       if args.mode == "recall" else "sparsity 0.8 + head tiers"),
+                   "layers_per_rank": 1, "l2": "inputs larger than L2 (Q,K,V = %.2f GB)" % (3 * q.numel() * 2 / 1e9)},
+        "ms_per_layer_sparse": round(k4_max / K, 3),
+        "search_overhead_ms": round((tk[1] + tk[2]) / K, 3),
+        "search_overhead_vs_dense": round((tk[1] + tk[2]) / tk[0], 4),
+        "dense_ms": round(ms[0], 3),
+        "kept_density": round(nnz / (H * nb * nb), 4),
+        "roofline": roof, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": hp.kernels_per_run() * K, "clocks": clocks,
+        "wall_s_timed_region": round(wall, 3),
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_reference(args):
+    """The oracle as the reference arm: each step runs the fp64 oracle hot path (dense attention ->
+    block mass -> recall selection -> masked attention) for a bounded sample of q-blocks of head 0."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    import workloads
+    lay = workloads.layout_for(args.config)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    q, k, v = workloads.generate_qkv(lay, device=dev)
+    qh, kh, vh = (x[0, 0].float().double().cpu().numpy() for x in (q, k, v))
+    del q, k, v
+    blocks = oracle.block_map(lay.n_video, lay.n_text, lay.block, lay.text_first)
+    nb = len(blocks)
+    scale = 1.0 / math.sqrt(lay.head_dim)
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
+    except Exception:  # noqa: BLE001
+        cores = os.cpu_count()
+    per_step = 3
+    stride = max(1, nb // 97)
+
+    def step(i):
+        ids = [((i * per_step + j) * stride) % nb for j in range(per_step)]
+        fl, t_sparse = 0.0, 0.0
+        for p in ids:
+            b = blocks[p]
+            rows = slice(b.start, b.start + b.length)
+            _, lse = oracle.dense_attention(qh[rows], kh, vh, scale)
+            lse_full = np.zeros(lay.n)
+            lse_full[rows] = lse
+            M = oracle.block_mass(qh, kh, lse_full, blocks, scale, q_block_ids=[p])[0]
+            forced, cands = oracle.row_forced_and_candidates(blocks, p, True)
+            kept = oracle.select_row_recall(M, forced, cands, args.recall)
+            t0 = time.perf_counter()
+            oracle.masked_attention(qh, kh, vh, blocks, {p: kept}, scale, q_block_ids=[p])
+            t_sparse += time.perf_counter() - t0
+            fl += 4.0 * lay.head_dim * b.length * sum(blocks[j].length for j in kept)
+        return fl, t_sparse
+
+    for i in range(args.warmup):
+        step(i)
+    fl, ts, t0 = 0.0, 0.0, time.perf_counter()
+    for i in range(args.steps):
+        a, b = step(args.warmup + i)
+        fl += a
+        ts += b
+    wall = time.perf_counter() - t0
+    val = fl / ts / 1e12
+    sample = (f"oracle hot path (fp64 numpy: dense+LSE, block mass, recall {args.recall} selection, masked "
+              f"attention) on {per_step} q-blocks of head 0 per step at {lay.name}; value = masked-attention "
+              f"TFLOP/s on kept blocks")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (workloads/synth.py, seeded)",
+        "config": {"workload": lay.name, "seq_len": lay.n, "heads": lay.heads, "head_dim": lay.head_dim,
+                   "block": lay.block, "selection": f"recall {args.recall} per head, text sink"},
+        "cpu_baseline": {"value": round(val, 6), "unit": UNIT, "cores": int(cores), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(val, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

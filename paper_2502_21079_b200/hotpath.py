@@ -1,0 +1,66 @@
+"""One pass of the AdaSpa hot path on fixed shapes:
+
+    K1 dense attention + LSE  ->  K2 block mass with that LSE  ->  K3 selection  ->  K4 sparse forward
+
+This is the search step t_w of the schedule (Alg. 1) followed by the
+block-sparse forward every later step runs.  Buffers are allocated once;
+`run()` accepts device tensors or (pinned) host tensors, in which case it stages them to the
+device on the same stream.  Everything runs through the C ABI; nothing here computes.
+"""
+
+import torch
+
+from . import _lib as L
+
+
+class HotPath:
+    def __init__(self, batch, heads, seq_len, head_dim, block_size, n_text, text_first=False,
+                 mode=L.SELECT_RECALL, targets=0.9, flags=L.FLAG_TEXT_SINK, tier_tau=0.8,
+                 softmax_scale=0.0, device="cuda"):
+        self.shape = (batch, heads, seq_len, head_dim)
+        self.kw = dict(block_size=block_size, n_text=n_text, text_first=text_first, softmax_scale=softmax_scale)
+        self.mode, self.flags, self.tier_tau = mode, flags, tier_tau
+        self.targets = [float(targets)] * heads if isinstance(targets, (int, float)) else [float(t) for t in targets]
+        dev = torch.device(device)
+        self.device = dev
+        e = lambda *s, dt=torch.bfloat16: torch.empty(*s, dtype=dt, device=dev)  # noqa: E731
+        self.q, self.k, self.v = e(*self.shape), e(*self.shape), e(*self.shape)
+        self.desc = L.make_desc(self.q, block_size, n_text, text_first, softmax_scale)
+        self.nb = L.num_blocks(self.desc)
+        self.o_dense = e(*self.shape)
+        self.o_sparse = e(*self.shape)
+        self.lse = e(batch, heads, seq_len, dt=torch.float32)
+        self.mass = e(batch, heads, self.nb, self.nb, dt=torch.float32)
+        rows = batch * heads * self.nb
+        self.csr = L.Csr(e(rows + 1, dt=torch.int32), e(rows * self.nb, dt=torch.int32), e(rows, dt=torch.int32),
+                         e(batch, heads, dt=torch.float32), e(batch, heads, dt=torch.int64))
+        self.ws = e(max(L.sparse_workspace_bytes(self.desc), 1), dt=torch.uint8)
+
+    def _stage(self, q, k, v):
+        if q.device == self.device:
+            return q, k, v
+        self.q.copy_(q, non_blocking=True)
+        self.k.copy_(k, non_blocking=True)
+        self.v.copy_(v, non_blocking=True)
+        return self.q, self.k, self.v
+
+    def run(self, q, k, v, events=None):
+        """events: optional list of 5 CUDA events recorded around K1, K2, K3, K4."""
+        q, k, v = self._stage(q, k, v)
+        rec = (lambda i: events[i].record()) if events else (lambda i: None)  # noqa: E731
+        rec(0)
+        L.dense_attn_lse(q, k, v, o=self.o_dense, lse=self.lse, **self.kw)
+        rec(1)
+        L.lse_cached_search(q, k, self.lse, block_mass=self.mass, **self.kw)
+        rec(2)
+        L.select_blocks(self.mass, heads_desc=self.desc, mode=self.mode, target=self.targets, flags=self.flags,
+                        tier_tau=self.tier_tau, out=self.csr)
+        rec(3)
+        L.block_sparse_attn(q, k, v, self.csr.row_ptr, self.csr.col_idx, o=self.o_sparse, workspace=self.ws,
+                            **self.kw)
+        rec(4)
+        return self.o_sparse
+
+    # launches of our kernels per run(): K1 1, K2 1, K3 3 (+2 with tiers), K4 3 (schedule + order + attention)
+    def kernels_per_run(self):
+        return 8 + (2 if self.flags & L.FLAG_HEAD_TIERS else 0)

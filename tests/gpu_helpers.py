@@ -13,8 +13,11 @@ O_MAX_ABS = 2e-2
 O_MEAN_ABS = 2e-3
 LSE_ABS = 1e-3
 TIE = 1e-6
-# K2 block mass: |dM| / |q-block| (fp32 S from the tensor core, fp32 exp2, fp64 reduction)
-MASS_REL = 2e-6
+# K2 block mass, |dM| / |q-block|.  Per element p = 2^x with x = fma(S, c, -lse*log2e):
+# fp32 S = q.k carries |S_raw| * 2^-24 rounding, i.e. |S_scaled| * 2^-24 in the exponent (natural units),
+# plus 2^-22 from ex2.approx and 2^-24 from the fma: at |S_scaled| <= 32 the relative error per element is
+# <= 32 * 2^-24 + 2^-22 + 2^-24 ~= 2.2e-6, and a block sum inherits it (all terms positive).  2.5x margin.
+MASS_REL = 5e-6
 
 
 def np64(t):

@@ -49,6 +49,10 @@ class Layout:
         return self.n_video + self.n_text
 
 
+# per-head sharpness range A_h (calibrated so that recall 0.9 keeps a mean block density
+# near the paper's default 1 - sparsity = 0.2 with a >= 5x spread across heads)
+SHARP = {"hyv110k": (2.75, 5.5), "hyv129f": (2.75, 5.5), "cogx45k": (2.75, 5.5)}
+
 CONFIGS = {
     "tiny": Layout("tiny", 7, 8, 8, 64, False, 2, 64, 64),
     "tiny_tf": Layout("tiny_tf", 7, 8, 8, 64, True, 2, 64, 64),
@@ -94,7 +98,7 @@ def _video_latent(lay, d, g, device):
     return _unit(0.8 * u_frame[t_idx] + 1.0 * u_tile[tile] + 0.6 * e)
 
 
-def generate_qkv(lay, batch=1, seed=BASE_SEED, device="cpu", sharp=(1.5, 4.0), sigma=0.0,
+def generate_qkv(lay, batch=1, seed=BASE_SEED, device="cpu", sharp=None, sigma=0.0,
                  step=0, heads=None, dtype=torch.bfloat16):
     """Q, K, V as bf16 [batch, H, N, d] (contiguous).  `heads` overrides lay.heads
     (e.g. a head shard).  Deterministic for a given (device type, arguments)."""
@@ -103,6 +107,8 @@ def generate_qkv(lay, batch=1, seed=BASE_SEED, device="cpu", sharp=(1.5, 4.0), s
     N = lay.n
     c = d ** 0.25
     out = [torch.empty(batch, H, N, d, dtype=dtype, device=device) for _ in range(3)]
+    if sharp is None:
+        sharp = SHARP.get(lay.name.split("_")[0], (1.5, 4.0))
     amps = sharpness(H, seed, *sharp)
     for b in range(batch):
         g = torch.Generator(device=device)
