@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libadaspa.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"{LIB_PATH} is missing: build it with `python -m paper_2502_21079_b200.build` "
+        f"{LIB_PATH} is missing: build it with `python paper_2502_21079_b200/build.py` "
         "(there is no CPU fallback for the AdaSpa kernels)")
 
 _lib = ctypes.CDLL(LIB_PATH)

@@ -1,6 +1,6 @@
 """Build libadaspa.so (all kernels + the C ABI) in-tree with nvcc for sm_100a.
 
-    python -m paper_2502_21079_b200.build [--verbose]
+    python paper_2502_21079_b200/build.py [--verbose]
 
 The .so lands next to this file so it travels with the repo snapshot to the GPU box.
 """
