@@ -160,7 +160,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
-
+  // 384 threads x 168 registers at launch; the producer/MMA warpgroup hands registers to the two
+  // softmax warpgroups, which hold a whole 128-column S row each (96*128 + 200*256 = 63488).
+  if (warp < 4) {
+  regs_dec<96>();
   if (warp == 0) {
     // ============================================================ TMA producer
     if (lane == 0) {
@@ -401,7 +404,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    regs_inc<200>();
     // ============================================================ softmax warps
     const int t = (warp - 4) >> 2;
     const int wq = warp & 3;                 // TMEM lane quarter
@@ -473,21 +478,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int lim0 = inf.lim[hq * 2 + 0];
       const int lim1 = inf.lim[hq * 2 + 1];
-      const bool full = (lim0 == 64 && lim1 == 128);
-      // pass 1: row max over the valid columns (S read from TMEM in 32-column chunks)
-      float mx = -INFINITY;
+      // the whole S row (128 fp32) in registers: one TMEM round trip per tile
+      uint32_t s[128];
+      tmem_ld32(s_addr + 0, s);
+      tmem_ld32(s_addr + 32, s + 32);
+      tmem_ld32(s_addr + 64, s + 64);
+      tmem_ld32(s_addr + 96, s + 96);
+      tmem_ld_wait32(s);
+      reg_fence32(s + 32);
+      reg_fence32(s + 64);
+      reg_fence32(s + 96);
+      if (!(lim0 == 64 && lim1 == 128)) {  // partial tile / unneeded half: those columns -> -inf
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld32(s_addr + c * 32, r);
-        tmem_ld_wait32(r);
-        const int lim = c < 2 ? lim0 : lim1;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float v = __uint_as_float(r[i]);
-          mx = (full || c * 32 + i < lim) ? fmaxf(mx, v) : mx;
+        for (int i = 0; i < 128; ++i) {
+          const int lim = i < 64 ? lim0 : lim1;
+          s[i] = i < lim ? s[i] : __float_as_uint(-INFINITY);
         }
       }
+      // row max: 8 independent FMNMX3 chains, then a short tree
+      float mx8[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) mx8[a] = fmaxf(__uint_as_float(s[a]), __uint_as_float(s[8 + a]));
+#pragma unroll
+      for (int i = 16; i < 128; i += 16) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a) mx8[a] = fmax3(mx8[a], __uint_as_float(s[i + a]), __uint_as_float(s[i + 8 + a]));
+      }
+      const float mx = fmaxf(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(fmax3(mx8[3], mx8[4], mx8[5]), mx8[6], mx8[7]));
       const float mx2 = mx * sl2;
       const float m_new = fmaxf(m_used, mx2);
       const bool grow = m_new > m_used + kRescaleThreshold;  // also true when m_used == -inf
@@ -500,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool rescale_o = grow && alpha != 0.0f && ntile > 0;
       if (__any_sync(0xffffffffu, rescale_o)) {
         const float a = rescale_o ? alpha : 1.0f;
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
           uint32_t r[32];
           tmem_ld32(o_addr + c * 32, r);
@@ -511,29 +528,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       const float mb = (m_used == -INFINITY) ? 0.0f : m_used;
-      // pass 2: P = 2^(S*scale*log2e - m), packed to bf16 pairs and written over the first 64
-      // columns of S_t (chunk c lands in columns [16c, 16c+16), already consumed).
-      float lsum = 0.0f;
+      // P = 2^(S*scale*log2e - m): FFMA2 for the argument, MUFU.EX2 for 3 of every 4 pairs and a
+      // degree-3 polynomial on the FMA pipe for the 4th (FA4-style exp offload; P is rounded to
+      // bf16, whose 2^-9 dwarfs the polynomial's 7.5e-5).  P is packed to bf16 pairs and written
+      // over the first 64 columns of S_t (chunk c lands in columns [16c, 16c+16)).
+      const float2 sl2v = make_float2(sl2, sl2);
+      const float2 nmb = make_float2(-mb, -mb);
+      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld32(s_addr + c * 32, r);
-        tmem_ld_wait32(r);
-        const int lim = c < 2 ? lim0 : lim1;
+        uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          float p0 = ex2_approx(fmaf(__uint_as_float(r[2 * i]), sl2, -mb));
-          float p1 = ex2_approx(fmaf(__uint_as_float(r[2 * i + 1]), sl2, -mb));
-          if (!full) {
-            p0 = (c * 32 + 2 * i < lim) ? p0 : 0.0f;
-            p1 = (c * 32 + 2 * i + 1 < lim) ? p1 : 0.0f;
+          const float2 x = ffma2(make_float2(__uint_as_float(s[32 * c + 2 * i]), __uint_as_float(s[32 * c + 2 * i + 1])),
+                                 sl2v, nmb);
+          float2 pv;
+          if ((i & 3) == 3) {
+            pv.x = exp2_poly<3>(x.x);
+            pv.y = exp2_poly<3>(x.y);
+          } else {
+            pv.x = ex2_approx(x.x);
+            pv.y = ex2_approx(x.y);
           }
-          lsum += p0 + p1;
-          r[i] = pack_bf16x2(p0, p1);
+          acc[i & 3] = fadd2(acc[i & 3], pv);
+          pk[i] = pack_bf16x2(pv.x, pv.y);
         }
-        tmem_st16(s_addr + c * 16, r);
+        tmem_st16(s_addr + c * 16, pk);
       }
-      l_sum += lsum;
+      const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+      const float2 a = fadd2(a01, a23);
+      l_sum += a.x + a.y;
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();

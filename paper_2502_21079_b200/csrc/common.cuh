@@ -219,6 +219,62 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// Packed fp32 pairs (FFMA2 / FADD2 on sm_100): one issue slot for two lanes of work.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
+        "l"(*reinterpret_cast<uint64_t*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+// 2^x on the FMA pipe (offloads MUFU.EX2): x = j + f with j = rint(x), f in [-1/2, 1/2];
+// 2^f by a minimax polynomial (relative error 7.5e-5 for degree 3, 2.3e-7 for degree 5 -- the
+// latter matches ex2.approx's 2^-22), scaled by 2^j through the exponent bits (one IMAD).
+// x is clamped at -126 (so the exponent add cannot wrap; the result is then <= 2^-126, the
+// range ex2.approx.ftz flushes to 0), so x = -inf gives a value below 2^-126.
+template <int DEG>
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;  // 1.5 * 2^23: low mantissa bits of t hold rint(x)
+  const float f = x - (t - 12582912.0f);
+  float p;
+  if (DEG == 3) {
+    p = fmaf(fmaf(fmaf(0.05517154932022095f, f, 0.2426111400127411f), f, 0.6932610273361206f), f,
+             0.9999280571937561f);
+  } else {
+    p = fmaf(fmaf(fmaf(fmaf(fmaf(0.001327645848505199f, f, 0.009675541892647743f), f, 0.05550713464617729f), f,
+                        0.24022120237350464f),
+                   f, 0.6931469440460205f),
+              f, 1.0000001192092896f);
+  }
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// Warpgroup register re-balancing (all 4 warps of a warpgroup execute the same instruction).
+template <int N>
+__device__ __forceinline__ void regs_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void regs_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

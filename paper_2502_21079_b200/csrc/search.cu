@@ -6,9 +6,11 @@
 // 128-row q tiles of one head (q-blocks 2p,2p+1 at B=128; 4p..4p+3 at B=64), the kv stream is
 // every kv tile of the head (one block at B=128, two at B=64).  S tiles are double-buffered
 // per q tile in TMEM (4 x 128 columns), so the tensor core runs ahead of the exp work.
-// Softmax-role threads own one row: x = fma(S, scale*log2e, -lse*log2e), p = 2^x, a pairwise
-// (tree) fp32 sum per kv block, then an fp64 cross-row reduction (warp shuffle + shared
-// memory) gives one fp32 mass per (q-block, kv-block).  S is never written to memory.
+// Exp-role threads own one row: x = fma(S, scale*log2e, -lse*log2e), p = 2^x (MUFU.EX2, one
+// pair in four on the FMA pipe), fp32 partial sums per kv block, a warp-shuffle sum over the
+// warp's 32 rows into shared memory, and every kChunk kv tiles one fixed-order fp64 sum over the
+// 4 warps of the q tile gives one fp32 mass per (q-block, kv-block) -- no per-tile barrier.
+// S is never written to memory.
 #include "attn.cuh"
 #include "common.cuh"
 
@@ -18,21 +20,23 @@ namespace {
 
 constexpr int kThreads = 384;
 
+constexpr int kChunk = 256;  // kv tiles per flush of the per-warp partial masses
+
 template <int D>
 struct SSmem {
   static constexpr int kTile = 128 * D * 2;
-  static constexpr int kNS = (D == 128) ? 5 : 11;
+  static constexpr int kNS = (D == 128) ? 4 : 8;
   static constexpr int kQ = 0;
   static constexpr int kK = 2 * kTile;
-  static constexpr int kBar = kK + kNS * kTile;
-  static constexpr int kBytes = kBar + 2048 + 1024;
+  static constexpr int kPart = kK + kNS * kTile;                  // float [2 tiles][4 warps][kChunk][2]
+  static constexpr int kBar = kPart + 2 * 4 * kChunk * 2 * 4;
+  static constexpr int kBytes = kBar + 1024 + 1024;
 };
 
 struct SBars {
-  uint64_t kv_full[12], kv_empty[12];
+  uint64_t kv_full[8], kv_empty[8];
   uint64_t q_full, q_empty;
   uint64_t s_full[2][2], s_empty[2][2];
-  double red[2][2][4][2];   // [tile][buf][warp quarter][kv half]
   uint32_t tmem_base;
 };
 
@@ -95,27 +99,32 @@ __device__ __forceinline__ void kv_tile(const SearchParams& p, bool two, int j, 
   }
 }
 
-// Pairwise sum of 2^x over 64 consecutive columns held in s[0..63] (fp32 bits); columns
-// at or beyond `lim` are excluded.
+// Sum of 2^x over 64 consecutive columns held in s[0..63] (fp32 bits), x = S*scale*log2e - lse*log2e
+// (reading R4); columns at or beyond `lim` are excluded.  The argument is one FFMA2 per pair; one
+// pair in four goes through the degree-5 polynomial on the FMA pipe (relative error 2.3e-7, the
+// same class as ex2.approx's 2^-22), the rest through MUFU.EX2; 4 packed partial sums, then a tree.
 template <bool FULL>
-__device__ __forceinline__ float half_mass(const uint32_t* s, float sl2, float nl, int lim) {
-  float v[32];
+__device__ __forceinline__ float half_mass(const uint32_t* s, float2 sl2, float2 nl, int lim) {
+  float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
-    float a = ex2_approx(fmaf(__uint_as_float(s[2 * i]), sl2, nl));
-    float b = ex2_approx(fmaf(__uint_as_float(s[2 * i + 1]), sl2, nl));
-    if (!FULL) {
-      a = (2 * i < lim) ? a : 0.0f;
-      b = (2 * i + 1 < lim) ? b : 0.0f;
+    const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sl2, nl);
+    float2 e;
+    if ((i & 3) == 3) {
+      e.x = exp2_poly<5>(x.x);
+      e.y = exp2_poly<5>(x.y);
+    } else {
+      e.x = ex2_approx(x.x);
+      e.y = ex2_approx(x.y);
     }
-    v[i] = a + b;
+    if (!FULL) {
+      e.x = (2 * i < lim) ? e.x : 0.0f;
+      e.y = (2 * i + 1 < lim) ? e.y : 0.0f;
+    }
+    acc[i & 3] = fadd2(acc[i & 3], e);
   }
-#pragma unroll
-  for (int w = 16; w >= 1; w >>= 1) {
-#pragma unroll
-    for (int i = 0; i < w; ++i) v[i] += v[i + w];
-  }
-  return v[0];
+  const float2 a = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+  return a.x + a.y;
 }
 
 template <int D, bool TWO>
@@ -131,6 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem + S::kQ;
   uint8_t* sK = smem + S::kK;
+  float* part = reinterpret_cast<float*>(smem + S::kPart);
   SBars* bars = reinterpret_cast<SBars*>(smem + S::kBar);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -161,6 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = bars->tmem_base;
   const int ntiles = p.kv_tiles;
 
+  if (warp < 4) {
+  regs_dec<96>();
   if (warp == 0) {
     if (lane == 0) {
       int slot = 0;
@@ -233,102 +245,108 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_commit(&bars->q_empty);
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    regs_inc<200>();
+    // ============================================================ exp / block-sum warps
     const int t = (warp - 4) >> 2;
     const int wq = warp & 3;
     const int row = wq * 32 + lane;
-    const int hq = wq >> 1;
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-    const float sl2 = p.scale_log2;
+    const float2 sl2v = make_float2(p.scale_log2, p.scale_log2);
     uint32_t sfph[2] = {0u, 0u};
     const int nb = p.grid.nb;
+    float* my_part = part + (t * 4 + wq) * kChunk * 2;   // this warp's [kChunk][2] partial masses
+    const float* grp_part = part + t * 4 * kChunk * 2;  // the 4 warps of this q tile
     for (int item = blockIdx.x; item < p.num_items; item += gridDim.x) {
       QTiles q;
       decode_search_item(p, TWO, item, q);
       if (!q.exists[t]) continue;
       int tok;
       bool rvalid;
-      int my_qb;
-      if (!TWO) {
+      if (!TWO || row < 64) {
         tok = q.start0[t] + row;
         rvalid = row < q.len0[t];
-        my_qb = q.qb0[t];
-      } else if (row < 64) {
-        tok = q.start0[t] + row;
-        rvalid = row < q.len0[t];
-        my_qb = q.qb0[t];
       } else {
         tok = q.start1[t] + row - 64;
         rvalid = (row - 64) < q.len1[t];
-        my_qb = q.qb1[t];
       }
       const float nl = rvalid ? -__ldg(p.lse + static_cast<int64_t>(q.bh) * p.N + tok) * kLog2e : 0.0f;
+      const float2 nlv = make_float2(nl, nl);
       float* mout = p.mass + static_cast<int64_t>(q.bh) * nb * nb;
-      for (int j = 0; j < ntiles; ++j) {
-        const int buf = j & 1;
-        int s0, l0, s1, l1, kb0, kb1;
-        kv_tile(p, TWO, j, s0, l0, s1, l1, kb0, kb1);
-        mbar_wait(&bars->s_full[t][buf], sfph[buf]);
-        sfph[buf] ^= 1;
-        tc_fence_after();
-        uint32_t s[128];
-        const uint32_t sa = tmem + lane_base + t * 256 + buf * 128;
-        tmem_ld32(sa + 0, s);
-        tmem_ld32(sa + 32, s + 32);
-        tmem_ld32(sa + 64, s + 64);
-        tmem_ld32(sa + 96, s + 96);
-        tmem_ld_wait32(s);
-        reg_fence32(s + 32);
-        reg_fence32(s + 64);
-        reg_fence32(s + 96);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars->s_empty[t][buf]);
-        // column limits of the two 64-column halves
-        int lim_a, lim_b;
-        if (!TWO) {
-          lim_a = l0 < 64 ? l0 : 64;
-          lim_b = l0 - 64;
-        } else {
-          lim_a = l0;
-          lim_b = l1;
-        }
-        float ma = (lim_a >= 64) ? half_mass<true>(s, sl2, nl, 64) : half_mass<false>(s, sl2, nl, lim_a);
-        float mb = (lim_b >= 64) ? half_mass<true>(s + 64, sl2, nl, 64)
-                                 : (lim_b > 0 ? half_mass<false>(s + 64, sl2, nl, lim_b) : 0.0f);
-        if (!rvalid) {
-          ma = 0.0f;
-          mb = 0.0f;
-        }
-        double da = ma, db = mb;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          da += __shfl_xor_sync(0xffffffffu, da, o);
-          db += __shfl_xor_sync(0xffffffffu, db, o);
-        }
-        if (lane == 0) {
-          bars->red[t][buf][wq][0] = da;
-          bars->red[t][buf][wq][1] = db;
-        }
-        named_bar_sync(1 + t, 128);
-        if (wq == 0 && lane < 4) {
-          const double(*r)[2] = bars->red[t][buf];
-          if (!TWO) {
-            if (lane == 0) {
-              const double m = ((r[0][0] + r[0][1]) + (r[1][0] + r[1][1])) + ((r[2][0] + r[2][1]) + (r[3][0] + r[3][1]));
-              mout[static_cast<int64_t>(my_qb) * nb + kb0] = static_cast<float>(m);
-            }
+      for (int j0 = 0; j0 < ntiles; j0 += kChunk) {
+        const int j1 = j0 + kChunk < ntiles ? j0 + kChunk : ntiles;
+        for (int j = j0; j < j1; ++j) {
+          const int buf = j & 1;
+          int s0, l0, s1, l1, kb0, kb1;
+          kv_tile(p, TWO, j, s0, l0, s1, l1, kb0, kb1);
+          mbar_wait(&bars->s_full[t][buf], sfph[buf]);
+          sfph[buf] ^= 1;
+          tc_fence_after();
+          uint32_t s[128];
+          const uint32_t sa = tmem + lane_base + t * 256 + buf * 128;
+          tmem_ld32(sa + 0, s);
+          tmem_ld32(sa + 32, s + 32);
+          tmem_ld32(sa + 64, s + 64);
+          tmem_ld32(sa + 96, s + 96);
+          tmem_ld_wait32(s);
+          reg_fence32(s + 32);
+          reg_fence32(s + 64);
+          reg_fence32(s + 96);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars->s_empty[t][buf]);
+          // column limits of the two 64-column halves (kv blocks kb0 / kb1 at B=64)
+          const int lim_a = TWO ? l0 : (l0 < 64 ? l0 : 64);
+          const int lim_b = TWO ? l1 : l0 - 64;
+          float ma, mb;
+          if (lim_a >= 64 && lim_b >= 64) {
+            ma = half_mass<true>(s, sl2v, nlv, 64);
+            mb = half_mass<true>(s + 64, sl2v, nlv, 64);
           } else {
-            const int qh = lane >> 1, hf = lane & 1;
-            const int qb = qh == 0 ? q.qb0[t] : q.qb1[t];
-            const int kb = hf == 0 ? kb0 : kb1;
-            if (qb >= 0 && kb >= 0)
-              mout[static_cast<int64_t>(qb) * nb + kb] = static_cast<float>(r[2 * qh][hf] + r[2 * qh + 1][hf]);
+            ma = half_mass<false>(s, sl2v, nlv, lim_a);
+            mb = lim_b > 0 ? half_mass<false>(s + 64, sl2v, nlv, lim_b) : 0.0f;
+          }
+          if (!rvalid) {
+            ma = 0.0f;
+            mb = 0.0f;
+          }
+          // warp sum of (ma, mb): after the first exchange lanes 0-15 carry ma, 16-31 carry mb
+          const bool hi = lane & 16;
+          float v = hi ? mb : ma;
+          v += __shfl_xor_sync(0xffffffffu, hi ? ma : mb, 16);
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if ((lane & 15) == 0) my_part[(j - j0) * 2 + (lane >> 4)] = v;
+        }
+        // flush the chunk: one fixed-order fp64 sum over the 4 warps per (q-block, kv-block)
+        named_bar_sync(1 + t, 128);
+        for (int jj = row; jj < j1 - j0; jj += 128) {
+          const int j = j0 + jj;
+          if (!TWO) {
+            double m = 0.0;
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+              m += (double)grp_part[(w * kChunk + jj) * 2] + (double)grp_part[(w * kChunk + jj) * 2 + 1];
+            mout[static_cast<int64_t>(q.qb0[t]) * nb + j] = static_cast<float>(m);
+          } else {
+#pragma unroll
+            for (int qh = 0; qh < 2; ++qh) {
+              const int qb = qh == 0 ? q.qb0[t] : q.qb1[t];
+              if (qb < 0) continue;
+#pragma unroll
+              for (int hf = 0; hf < 2; ++hf) {
+                const int kb = 2 * j + hf;
+                if (kb >= nb) continue;
+                const double m = (double)grp_part[((2 * qh) * kChunk + jj) * 2 + hf] +
+                                 (double)grp_part[((2 * qh + 1) * kChunk + jj) * 2 + hf];
+                mout[static_cast<int64_t>(qb) * nb + kb] = static_cast<float>(m);
+              }
+            }
           }
         }
+        named_bar_sync(1 + t, 128);
       }
-      (void)my_qb;
-      (void)hq;
     }
   }
 

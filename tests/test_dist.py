@@ -1,0 +1,79 @@
+"""Multi-process host logic of the head sharding / Ulysses exchange, on CPU with
+the gloo backend at world size 2 and 3 (ragged token chunks)."""
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2502_21079_b200 import dist as D
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, N, H, d, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(5)
+        full = torch.randn(N, H, d, generator=g)          # the global [N, H, d] activation
+        sizes = D.seq_splits(N, world)
+        off = sum(sizes[:rank])
+        local = full[off:off + sizes[rank]].contiguous()   # this rank's token chunk
+        got = D.ulysses_in(local)
+        Hp = H // world
+        want = full[:, rank * Hp:(rank + 1) * Hp]
+        ok_in = torch.equal(got, want)
+        v = D.as_bhnd(got)
+        ok_view = (tuple(v.shape) == (1, Hp, N, d) and v.stride(2) == Hp * d and v.stride(1) == d
+                   and torch.equal(v[0, 1 % Hp], full[:, rank * Hp + 1 % Hp]))
+        back = D.ulysses_out(got * 2.0, sizes)
+        ok_out = torch.equal(back, 2.0 * local)
+        q.put((rank, ok_in, ok_view, ok_out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,N", [(2, 64), (3, 50)])
+def test_ulysses_roundtrip_gloo(world, N):
+    H, d = 6, 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, N, H, d, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok_in, ok_view, ok_out in res:
+        assert ok_in and ok_view and ok_out, (rank, ok_in, ok_view, ok_out)
+
+
+def test_head_range_partitions():
+    for H in (1, 5, 24, 48):
+        for w in (1, 2, 3, 8):
+            rs = [D.head_range(H, w, r) for r in range(w)]
+            assert rs[0][0] == 0 and rs[-1][1] == H
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(w - 1))
+            assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
+
+
+def test_lpt_assign():
+    costs = [9, 1, 1, 1, 8, 2, 7, 3]
+    parts = D.lpt_assign(costs, 3)
+    assert sorted(h for p in parts for h in p) == list(range(8))
+    loads = [sum(costs[h] for h in p) for p in parts]
+    assert max(loads) - min(loads) <= max(costs)
+    assert max(loads) <= sum(costs) / 3 + max(costs)
