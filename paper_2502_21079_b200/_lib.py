@@ -12,7 +12,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libadaspa.so")
+LIB_PATH = os.environ.get("ADASPA_LIB") or os.path.join(_HERE, "libadaspa.so")  # override: diagnostic builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -27,12 +27,45 @@
 
 namespace adaspa {
 
+#ifdef ADASPA_TRACE
+// Diagnostic build only (-DADASPA_TRACE): per-tile clock64 stamps of CTA 0 -- softmax warp 4
+// (q tile 0, column half 0) events 0..3 and the MMA issuer's events -- read back through
+// adaspa_debug_trace().  The product library is built without it.
+__device__ unsigned long long g_trace[2][4096];
+__device__ int g_trace_n[2];
+#define ADASPA_TRACE_EV(k)                                                                    \
+  do {                                                                                        \
+    if (blockIdx.x == 0 && warp == 4 && lane == 0 && tr_k < 1000) g_trace[0][tr_k * 4 + (k)] = clock64(); \
+    if ((k) == 3) ++tr_k;                                                                     \
+  } while (0)
+#define ADASPA_TRACE_MMA(k)                                                                   \
+  do {                                                                                        \
+    if (blockIdx.x == 0 && tr_n < 1000) g_trace[1][tr_n * 4 + (k)] = clock64();               \
+    if ((k) == 3) ++tr_n;                                                                     \
+  } while (0)
+#else
+#define ADASPA_TRACE_EV(k) \
+  do {                     \
+  } while (0)
+#define ADASPA_TRACE_MMA(k) \
+  do {                      \
+  } while (0)
+#endif
+
 namespace {
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 640;
 __device__ __forceinline__ uint32_t s_col(int t) { return static_cast<uint32_t>(t) * 128u; }
 __device__ __forceinline__ uint32_t o_col(int t) { return 256u + static_cast<uint32_t>(t) * 128u; }
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef ADASPA_EXP_POLY_MOD
+#define ADASPA_EXP_POLY_MOD 0
+#endif
+#ifndef ADASPA_EXP_PACKED
+#define ADASPA_EXP_PACKED 1
+#endif
+constexpr int kExpPolyMod = ADASPA_EXP_POLY_MOD;  // one pair in kExpPolyMod on the FMA-pipe polynomial (0: none)
+constexpr bool kExpPacked = ADASPA_EXP_PACKED;   // FFMA2/FADD2 for the argument and the row sum
 
 enum : int { kNormal = 0, kEnd = 1, kAllEnd = 2 };
 
@@ -57,11 +90,11 @@ struct ItemInfo {
 template <int D>
 struct Smem {
   static constexpr int kTile = 128 * D * 2;  // one 128-row tile of d bf16 columns
-  static constexpr int kNS = (D == 128) ? 5 : 10;
+  static constexpr int kNS = (D == 128) ? 4 : 10;
   static constexpr int kQ = 0;
   static constexpr int kKV = 2 * kTile;
   static constexpr int kBar = kKV + kNS * kTile;
-  static constexpr int kBytes = kBar + 1024 + 1024;  // barriers/meta + alignment slack
+  static constexpr int kBytes = kBar + 6144 + 1024;  // barriers/meta/exchange + alignment slack
 };
 
 struct Bars {
@@ -72,6 +105,8 @@ struct Bars {
   TileInfo info[2][2];
   ItemInfo qitem;
   uint32_t tmem_base;
+  float xm[2][2 * 128];  // per q tile: row-max of column half 0 | half 1
+  float xl[2][2 * 128];  // per q tile: row-sum of column half 0 | half 1
 };
 
 __device__ __forceinline__ void decode_item(const AttnParams& p, bool sparse, bool two, int id, ItemInfo& it) {
@@ -126,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int CH = D / 64;            // 64-column (128-byte) chunks per row
   constexpr int CHUNK = 128 * 128;      // bytes per chunk of a 128-row tile
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared pointer
   uint8_t* sQ = smem + S::kQ;
   uint8_t* sKV = smem + S::kKV;
   Bars* bars = reinterpret_cast<Bars*>(smem + S::kBar);
@@ -143,9 +178,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars->q_empty, 1);
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bars->s_full[t], 2);
-      mbar_init(&bars->p_full[t], 4);
+      mbar_init(&bars->p_full[t], 8);
       mbar_init(&bars->o_full[t], 1);
-      mbar_init(&bars->o_empty[t], 4);
+      mbar_init(&bars->o_empty[t], 8);
     }
     fence_mbar_init();
     tma_prefetch_desc(&tq);
@@ -160,10 +195,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
-  // 384 threads x 168 registers at launch; the producer/MMA warpgroup hands registers to the two
-  // softmax warpgroups, which hold a whole 128-column S row each (96*128 + 200*256 = 63488).
+  // 640 threads x 96 registers at launch; the producer/MMA warpgroup hands registers to the four
+  // softmax warpgroups, which hold a 64-column half S row each.  The pool is what the launch
+  // allocated, 640 x 96: 64*128 + 104*512 = 61440 (setmaxnreg.inc beyond it never returns).
   if (warp < 4) {
-  regs_dec<96>();
+  regs_dec<64>();
   if (warp == 0) {
     // ============================================================ TMA producer
     if (lane == 0) {
@@ -260,6 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t pph[2] = {0u, 0u}, oeph[2] = {0u, 0u};
       int icnt[2] = {0, 0};
       bool o_dirty[2] = {false, false};
+      int tr_n = 0;
+      (void)tr_n;
 
       auto issue_qk = [&](int t, int kslot) {
 #pragma unroll
@@ -360,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (pend[t]) {
               mbar_wait(&bars->p_full[t], pph[t]);
               pph[t] ^= 1;
+              ADASPA_TRACE_MMA(t * 2 + 0);
               tc_fence_after();
               if (first_pv[t] && o_dirty[t]) {
                 mbar_wait(&bars->o_empty[t], oeph[t]);
@@ -374,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t need = (static_cast<uint32_t>(mt.mask) >> (4 * t)) & 0xFu;
             if (need) {
               issue_qk(t, kslot);
+              ADASPA_TRACE_MMA(t * 2 + 1);
               TileInfo& inf = bars->info[t][icnt[t] & 1];
               ++icnt[t];
               inf.kind = kNormal;
@@ -406,23 +446,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   } else {
-    regs_inc<200>();
+    regs_inc<104>();
     // ============================================================ softmax warps
-    const int t = (warp - 4) >> 2;
-    const int wq = warp & 3;                 // TMEM lane quarter
+    // warps 4..19: sw = warp - 4, q tile t = sw >> 3, column half hc = (sw >> 2) & 1, TMEM lane
+    // quarter wq = warp & 3.  Two warps (one per column half) share each row: 2 warps per SMSP
+    // per q tile, so one warp's dependency stalls are covered by the other's work.
+    const int sw = warp - 4;
+    const int t = sw >> 3;
+    const int hc = (sw >> 2) & 1;
+    const int wq = warp & 3;
     const int row = wq * 32 + lane;          // row of the q tile (TMEM lane)
     const int hq = wq >> 1;                  // 64-row half
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t s_addr = tmem + lane_base + s_col(t);
-    const uint32_t o_addr = tmem + lane_base + o_col(t);
+    const uint32_t o_addr = tmem + lane_base + o_col(t) + hc * (D / 2);
+    float* xm = bars->xm[t];                 // [2][128] row-max exchange
+    float* xl = bars->xl[t];                 // [2][128] row-sum exchange
     const float sl2 = p.scale_log2;
     uint32_t sph = 0, oph = 0;
     int icnt = 0;
     float m_used = -INFINITY, l_sum = 0.0f;
     int ntile = 0;
+    int tr_k = 0;
+    (void)tr_k;
+    const Poly4x2 poly;
     for (;;) {
       mbar_wait(&bars->s_full[t], sph);
       sph ^= 1;
+      ADASPA_TRACE_EV(0);
       tc_fence_after();
       const TileInfo& inf = bars->info[t][icnt & 1];
       ++icnt;
@@ -443,13 +494,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             tok = inf.start1 + row - 64;
             valid = row - 64 < inf.len1;
           }
+          xl[hc * 128 + row] = l_sum;
+          named_bar_sync(1 + t, 256);
+          const float l_tot = l_sum + xl[(1 - hc) * 128 + row];
           mbar_wait(&bars->o_full[t], oph);
           oph ^= 1;
           tc_fence_after();
-          const float inv = l_sum > 0.0f ? 1.0f / l_sum : 0.0f;
-          __nv_bfloat16* optr = p.o + b * p.sb + h * p.sh + static_cast<int64_t>(tok) * p.sn;
+          const float inv = l_tot > 0.0f ? 1.0f / l_tot : 0.0f;
+          __nv_bfloat16* optr = p.o + b * p.sb + h * p.sh + static_cast<int64_t>(tok) * p.sn + hc * (D / 2);
 #pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
+          for (int c = 0; c < D / 64; ++c) {
             uint32_t r[32];
             tmem_ld32(o_addr + c * 32, r);
             tmem_ld_wait32(r);
@@ -463,8 +517,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
             }
           }
-          if (valid && p.lse) {
-            const float lv = l_sum > 0.0f ? (m_used + __log2f(l_sum)) * kLn2 : -INFINITY;
+          if (hc == 0 && valid && p.lse) {
+            const float lv = l_tot > 0.0f ? (m_used + __log2f(l_tot)) * kLn2 : -INFINITY;
             p.lse[(static_cast<int64_t>(b) * p.H + h) * p.N + tok] = lv;
           }
           tc_fence_before();
@@ -476,35 +530,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         ntile = 0;
         continue;
       }
-      const int lim0 = inf.lim[hq * 2 + 0];
-      const int lim1 = inf.lim[hq * 2 + 1];
-      // the whole S row (128 fp32) in registers: one TMEM round trip per tile
-      uint32_t s[128];
-      tmem_ld32(s_addr + 0, s);
-      tmem_ld32(s_addr + 32, s + 32);
-      tmem_ld32(s_addr + 64, s + 64);
-      tmem_ld32(s_addr + 96, s + 96);
+      // my 64 columns [64hc, 64hc+64): valid below `lim` (relative)
+      const int lim = hc == 0 ? inf.lim[hq * 2 + 0] : inf.lim[hq * 2 + 1] - 64;
+      uint32_t s[64];
+      tmem_ld32(s_addr + hc * 64, s);
+      tmem_ld32(s_addr + hc * 64 + 32, s + 32);
       tmem_ld_wait32(s);
       reg_fence32(s + 32);
-      reg_fence32(s + 64);
-      reg_fence32(s + 96);
-      if (!(lim0 == 64 && lim1 == 128)) {  // partial tile / unneeded half: those columns -> -inf
+      ADASPA_TRACE_EV(1);
+      if (lim < 64) {  // partial tile / unneeded half: those columns -> -inf
 #pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          const int lim = i < 64 ? lim0 : lim1;
-          s[i] = i < lim ? s[i] : __float_as_uint(-INFINITY);
-        }
+        for (int i = 0; i < 64; ++i) s[i] = i < lim ? s[i] : __float_as_uint(-INFINITY);
       }
-      // row max: 8 independent FMNMX3 chains, then a short tree
-      float mx8[8];
+      float mx4[4];
 #pragma unroll
-      for (int a = 0; a < 8; ++a) mx8[a] = fmaxf(__uint_as_float(s[a]), __uint_as_float(s[8 + a]));
+      for (int a = 0; a < 4; ++a) mx4[a] = fmaxf(__uint_as_float(s[a]), __uint_as_float(s[4 + a]));
 #pragma unroll
-      for (int i = 16; i < 128; i += 16) {
+      for (int i = 8; i < 64; i += 8) {
 #pragma unroll
-        for (int a = 0; a < 8; ++a) mx8[a] = fmax3(mx8[a], __uint_as_float(s[i + a]), __uint_as_float(s[i + 8 + a]));
+        for (int a = 0; a < 4; ++a) mx4[a] = fmax3(mx4[a], __uint_as_float(s[i + a]), __uint_as_float(s[i + 4 + a]));
       }
-      const float mx = fmaxf(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(fmax3(mx8[3], mx8[4], mx8[5]), mx8[6], mx8[7]));
+      const float lmx = fmax3(mx4[0], mx4[1], fmaxf(mx4[2], mx4[3]));
+      // the partner warp holds the other 64 columns of the same rows; the barrier also orders
+      // both halves' TMEM loads of S before either overwrites S columns with P
+      xm[hc * 128 + row] = lmx;
+      named_bar_sync(1 + t, 256);
+      ADASPA_TRACE_EV(2);
+      const float mx = fmaxf(lmx, xm[(1 - hc) * 128 + row]);
       const float mx2 = mx * sl2;
       const float m_new = fmaxf(m_used, mx2);
       const bool grow = m_new > m_used + kRescaleThreshold;  // also true when m_used == -inf
@@ -518,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (__any_sync(0xffffffffu, rescale_o)) {
         const float a = rescale_o ? alpha : 1.0f;
 #pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < D / 64; ++c) {
           uint32_t r[32];
           tmem_ld32(o_addr + c * 32, r);
           tmem_ld_wait32(r);
@@ -529,31 +581,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const float mb = (m_used == -INFINITY) ? 0.0f : m_used;
       // P = 2^(S*scale*log2e - m): FFMA2 for the argument, MUFU.EX2 for 3 of every 4 pairs and a
-      // degree-3 polynomial on the FMA pipe for the 4th (FA4-style exp offload; P is rounded to
-      // bf16, whose 2^-9 dwarfs the polynomial's 7.5e-5).  P is packed to bf16 pairs and written
-      // over the first 64 columns of S_t (chunk c lands in columns [16c, 16c+16)).
+      // packed degree-4 polynomial on the FMA pipe for the 4th (exp offload; it keeps the LSE --
+      // the search's cache -- at MUFU accuracy).  P is packed to bf16 pairs: S column c of this
+      // half lands in P column 32hc + c/2 (the P of a tile occupies S columns [0, 64)).
       const float2 sl2v = make_float2(sl2, sl2);
       const float2 nmb = make_float2(-mb, -mb);
       float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float2 x = ffma2(make_float2(__uint_as_float(s[32 * c + 2 * i]), __uint_as_float(s[32 * c + 2 * i + 1])),
-                                 sl2v, nmb);
+          const float s0 = __uint_as_float(s[32 * c + 2 * i]), s1 = __uint_as_float(s[32 * c + 2 * i + 1]);
+          float2 x;
+          if (kExpPacked) {
+            x = ffma2(make_float2(s0, s1), sl2v, nmb);
+          } else {
+            x.x = fmaf(s0, sl2, -mb);
+            x.y = fmaf(s1, sl2, -mb);
+          }
           float2 pv;
-          if ((i & 3) == 3) {
-            pv.x = exp2_poly<3>(x.x);
-            pv.y = exp2_poly<3>(x.y);
+          if (kExpPolyMod > 0 && (i % (kExpPolyMod > 0 ? kExpPolyMod : 1)) == kExpPolyMod - 1) {
+            pv = exp2_poly4x2(x, poly);
           } else {
             pv.x = ex2_approx(x.x);
             pv.y = ex2_approx(x.y);
           }
-          acc[i & 3] = fadd2(acc[i & 3], pv);
+          if (kExpPacked) {
+            acc[i & 3] = fadd2(acc[i & 3], pv);
+          } else {
+            acc[i & 3].x += pv.x;
+            acc[i & 3].y += pv.y;
+          }
           pk[i] = pack_bf16x2(pv.x, pv.y);
         }
-        tmem_st16(s_addr + c * 16, pk);
+        tmem_st16(s_addr + hc * 32 + c * 16, pk);
       }
       const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
       const float2 a = fadd2(a01, a23);
@@ -561,6 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
+      ADASPA_TRACE_EV(3);
       if (lane == 0) mbar_arrive(&bars->p_full[t]);
       ++ntile;
     }
@@ -674,6 +737,13 @@ __global__ void __launch_bounds__(256) sparse_order_kernel(SparsePrepParams p) {
 }
 
 }  // namespace
+
+#ifdef ADASPA_TRACE
+extern "C" int adaspa_debug_trace(unsigned long long* host, int n) {
+  if (cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * (n < 8192 ? n : 8192)) != cudaSuccess) return -1;
+  return 0;
+}
+#endif
 
 cudaError_t launch_sparse_prep(const SparsePrepParams& p, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(p.stream, 0, sizeof(uint32_t) * static_cast<size_t>(p.num_items) * p.stream_stride, st);

@@ -1,0 +1,48 @@
+"""Per-tile clock64 trace of K1 on one config (diagnostic build, see ADASPA_TRACE in attn_fwd.cu).
+    nvcc ... -DADASPA_TRACE -o /tmp/libadaspa_trace.so && ADASPA_LIB=/tmp/libadaspa_trace.so python tools/trace_probe.py
+"""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import workloads
+import paper_2502_21079_b200 as ada
+from paper_2502_21079_b200 import _lib
+
+name = sys.argv[1] if len(sys.argv) > 1 else "hyv110k"
+which = sys.argv[2] if len(sys.argv) > 2 else "dense"
+lay = workloads.layout_for(name)
+q, k, v = workloads.generate_qkv(lay, device="cuda")
+kw = dict(block_size=lay.block, n_text=lay.n_text, text_first=lay.text_first)
+o, lse = ada.dense_attn_lse(q, k, v, **kw)
+if which == "sparse":
+    M = ada.lse_cached_search(q, k, lse, **kw)
+    desc = ada.make_desc(q, lay.block, lay.n_text, lay.text_first)
+    out = ada.select_blocks(M, heads_desc=desc, mode=ada.SELECT_RECALL, target=[0.9] * lay.heads)
+    ada.block_sparse_attn(q, k, v, out.row_ptr, out.col_idx, **kw)
+torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * 8192)()
+assert _lib._lib.adaspa_debug_trace(buf, 8192) == 0
+a = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
+sm = a[:4000].reshape(1000, 4)
+mm = a[4096:4096 + 4000].reshape(1000, 4)
+n = int((sm[:, 3] > 0).sum())
+sm = sm[:n]
+print(f"{name} {which}: softmax warp 4 (tile 0, half 0), {n} tiles")
+ld = sm[:, 1] - sm[:, 0]; mx = sm[:, 2] - sm[:, 1]; ex = sm[:, 3] - sm[:, 2]
+wait = sm[1:, 0] - sm[:-1, 3]; period = np.diff(sm[:, 0])
+for nm, x in (("LDTM", ld), ("max+xchg barrier", mx), ("rescale+exp+P store", ex), ("wait for next S", wait), ("period", period)):
+    x = x[10:-10] if len(x) > 40 else x
+    print(f"  {nm:22s} median {np.median(x):8.0f}  p10 {np.percentile(x,10):8.0f}  p90 {np.percentile(x,90):8.0f}")
+m = int((mm[:, 3] > 0).sum())
+mm = mm[:m]
+print(f"MMA issuer: {m} entries")
+names = ["p_full0 seen", "QK0 issued", "p_full1 seen", "QK1 issued"]
+for i in range(4):
+    d = np.diff(mm[:, i])[10:-10]
+    print(f"  period of '{names[i]}': median {np.median(d):.0f}")
+for i, j in ((0, 1), (1, 2), (2, 3)):
+    d = (mm[:, j] - mm[:, i])[10:-10]
+    print(f"  '{names[i]}' -> '{names[j]}': median {np.median(d):.0f}  p90 {np.percentile(d,90):.0f}")
+d = (mm[1:, 0] - mm[:-1, 3])[10:-10]
+print(f"  'QK1 issued' -> next 'p_full0 seen': median {np.median(d):.0f}")
