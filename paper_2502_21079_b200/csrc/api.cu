@@ -120,7 +120,7 @@ adaspa_status make_map(CUtensorMap* map, const void* base, const adaspa_attn_des
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct SelectWs {
-  size_t bits, nnz, kept, total, kbh, bytes;
+  size_t bits, nnz, kept, total, kbh, loff, hcnt, hbase, hist, bytes;
 };
 SelectWs select_ws_layout(const adaspa_attn_desc* d) {
   const BlockGrid g = make_grid(d);
@@ -133,6 +133,10 @@ SelectWs select_ws_layout(const adaspa_attn_desc* d) {
   w.kept = off; off = align256(off + rows * 8);
   w.total = off; off = align256(off + rows * 8);
   w.kbh = off; off = align256(off + (size_t)d->batch * d->heads * 4);
+  w.loff = off; off = align256(off + rows * 4);
+  w.hcnt = off; off = align256(off + (size_t)d->batch * d->heads * 4);
+  w.hbase = off; off = align256(off + (size_t)d->batch * d->heads * 4);
+  w.hist = off; off = align256(off + (size_t)(g.nb + 1) * 4);
   w.bytes = off;
   return w;
 }
@@ -320,6 +324,10 @@ adaspa_status adaspa_select_blocks(const adaspa_attn_desc* desc, const float* bl
   fp.row_nnz = rp.row_nnz;
   fp.row_kept = rp.row_kept;
   fp.row_total = rp.row_total;
+  fp.local_off = reinterpret_cast<int*>(ws + w.loff);
+  fp.head_cnt = reinterpret_cast<int*>(ws + w.hcnt);
+  fp.head_base = reinterpret_cast<int*>(ws + w.hbase);
+  fp.hist = reinterpret_cast<int*>(ws + w.hist);
   fp.row_ptr = row_ptr;
   fp.row_order = row_order;
   fp.head_recall = head_recall;
@@ -327,8 +335,14 @@ adaspa_status adaspa_select_blocks(const adaspa_attn_desc* desc, const float* bl
   SelectWriteParams& wp = L.wr;
   wp.rows = rp.rows;
   wp.nwords = rp.nwords;
+  wp.nb = g.nb;
   wp.bits = rp.bits;
+  wp.row_nnz = rp.row_nnz;
+  wp.local_off = fp.local_off;
+  wp.head_base = fp.head_base;
+  wp.hist = fp.hist;
   wp.row_ptr = row_ptr;
+  wp.row_order = row_order;
   wp.col_idx = col_idx;
   cudaError_t e = launch_select(L, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "select_blocks launch");

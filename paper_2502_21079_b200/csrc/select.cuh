@@ -40,6 +40,10 @@ struct SelectFinalParams {
   const int* row_nnz;
   const double* row_kept;
   const double* row_total;
+  int* local_off;         // [rows]   exclusive offset of a row within its head
+  int* head_cnt;          // [B*H]    kept blocks per head
+  int* head_base;         // [B*H]    exclusive offset of a head in col_idx
+  int* hist;              // [nb+1]   row-count histogram -> LPT slots
   int32_t* row_ptr;
   int32_t* row_order;     // may be null
   float* head_recall;     // may be null
@@ -47,9 +51,14 @@ struct SelectFinalParams {
 };
 
 struct SelectWriteParams {
-  int rows, nwords;
+  int rows, nwords, nb;
   const uint32_t* bits;
-  const int32_t* row_ptr;
+  const int* row_nnz;
+  const int* local_off;
+  const int* head_base;
+  int* hist;
+  int32_t* row_ptr;
+  int32_t* row_order;     // may be null
   int32_t* col_idx;
 };
 

@@ -61,6 +61,7 @@ class HotPath:
         rec(4)
         return self.o_sparse
 
-    # launches of our kernels per run(): K1 1, K2 1, K3 3 (+2 with tiers), K4 3 (schedule + order + attention)
+    # launches of our kernels per run(): K1 1, K2 1, K3 4 (rows, head, scan, write; +2 with tiers),
+    # K4 3 (stream + order + attention)
     def kernels_per_run(self):
-        return 8 + (2 if self.flags & L.FLAG_HEAD_TIERS else 0)
+        return 9 + (2 if self.flags & L.FLAG_HEAD_TIERS else 0)
