@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ulysses", action="store_true",
+                    help="BASELINE configs[3]: one layer, sequence-sharded activations, NCCL all-to-all to "
+                         "head shards, K1..K4 on H/N heads per rank, all-to-all of O back (strong scaling)")
     return ap.parse_args()
 
 
@@ -240,22 +243,22 @@ def run_ours(args):
     K = args.steps
     value = work.item() * K / (k4_max / 1e3) / 1e12
 
-    # e2e: the same metric through the public API with host buffers (pinned), copies timed
+    # e2e: the same metric (K4 TFLOP/s on kept blocks) for a sparse step end to end through the public
+    # API from pinned host buffers: H2D of Q,K,V, the block-sparse forward on the cached CSR, D2H of O,
+    # pipelined over head groups (HotPath.run_sparse_host)
     e2e = None
     if not args.no_e2e:
         qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
         oh = torch.empty_like(qh).pin_memory()
         for _ in range(2):
-            hp.run(qh, kh, vh)
-            oh.copy_(hp.o_sparse, non_blocking=True)
+            hp.run_sparse_host(qh, kh, vh, oh)
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if ws > 1:
             torch.distributed.barrier()
         s0.record()
         for _ in range(K):
-            hp.run(qh, kh, vh)
-            oh.copy_(hp.o_sparse, non_blocking=True)
+            hp.run_sparse_host(qh, kh, vh, oh)
         s1.record()
         torch.cuda.synchronize()
         te = torch.tensor([s0.elapsed_time(s1)], dtype=torch.float64, device=dev)
@@ -265,7 +268,8 @@ def run_ours(args):
                "h2d_bytes_per_step": 3 * q.numel() * q.element_size(),
                "d2h_bytes_per_step": q.numel() * q.element_size(),
                "ms_per_step": round(te.item() / K, 3),
-               "note": "TFLOP/s on kept blocks over the whole step incl. H2D of Q,K,V and D2H of O (pinned)"}
+               "note": "sparse step from pinned host memory: H2D Q,K,V + K4 (cached CSR) + D2H O, "
+                       "overlapped over 4 head groups; TFLOP/s on kept blocks"}
 
     if rank != 0:
         if ws > 1:
@@ -318,6 +322,95 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def run_ulysses(args):
+    """configs[3]: ONE HunyuanVideo-shaped layer whose activations arrive sequence-sharded ([N/P, H, d]
+    per rank, as a sequence-parallel DiT holds them).  A step = NCCL all_to_all of Q, K, V to head shards
+    [N, H/P, d] -> K1 -> K2 -> K3 -> K4 on the local heads (token-major, read through the descriptor
+    strides: no unpack) -> all_to_all of O back.  value = kept FLOPs of the whole layer / max over ranks
+    of the K4 time (strong scaling)."""
+    ws, rank, local = dist_env()
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1,
+                                device_id=torch.device("cuda", local))
+    import workloads
+    import paper_2502_21079_b200 as ada
+    from paper_2502_21079_b200 import dist as D
+    from paper_2502_21079_b200.hotpath import HotPath
+    lay = workloads.layout_for(args.config)
+    dev = torch.device("cuda", local)
+    H, N, d = lay.heads, lay.n, lay.head_dim
+    if H % ws:
+        raise SystemExit(f"--ulysses needs heads ({H}) divisible by the world size ({ws})")
+    Hp = H // ws
+    sizes = D.seq_splits(N, ws)
+    off = sum(sizes[:rank])
+    q, k, v = workloads.generate_qkv(lay, device=dev)            # the global layer (same seed on every rank)
+    loc = [x[0].transpose(0, 1)[off:off + sizes[rank]].contiguous() for x in (q, k, v)]   # [N_p, H, d]
+    del q, k, v
+    torch.cuda.empty_cache()
+    hp = HotPath(1, Hp, N, d, lay.block, lay.n_text, lay.text_first, mode=ada.SELECT_RECALL,
+                 targets=args.recall, flags=ada.FLAG_TEXT_SINK, token_major=True)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record()
+        sh = [D.as_bhnd(D.ulysses_in(x, sizes=sizes)) for x in loc]             # [1, Hp, N, d] token-major views
+        if ev:
+            ev[1].record()
+        ev4 = ev[1:6] if ev else None
+        o = hp.run(*sh, events=ev4)
+        o_loc = D.ulysses_out(o[0].transpose(0, 1), sizes)          # [N_p, H, d]
+        if ev:
+            ev[6].record()
+        return o_loc
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(K)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(dev.index)
+    for i in range(K):
+        step(evs[i])
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = clk.stop()
+    # per step: a2a in, K1, K2, K3, K4, a2a out
+    per = [[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]), e[3].elapsed_time(e[4]),
+            e[4].elapsed_time(e[5]), e[5].elapsed_time(e[6])] for e in evs]
+    tk = [sum(p[i] for p in per) for i in range(6)]
+    total = sum(tk)
+    kfl, nnz = kept_flops(workloads.layout_for(args.config, heads=Hp), hp.csr, d)
+    t = torch.tensor([total] + tk, dtype=torch.float64, device=dev)
+    work = torch.tensor([kfl, float(nnz)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(work, op=dist.ReduceOp.SUM)
+    if rank == 0:
+        ms = [x / K for x in t.tolist()]
+        line = {
+            "metric": METRIC, "value": round(work[0].item() * K / (t[5].item() / 1e3) / 1e12, 3), "unit": UNIT,
+            "n_gpus": ws, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms[0], 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (workloads/synth.py, seeded; DESIGN.md \u00a75)",
+            "config": {"workload": lay.name + "-ulysses", "seq_len": N, "heads": H, "heads_per_rank": Hp,
+                       "head_dim": d, "block": lay.block, "parallelism": f"ulysses a2a x{ws} (NCCL)",
+                       "l2": "inputs larger than L2"},
+            "ms_per_layer_sparse": round(ms[5], 3), "a2a_in_ms": round(ms[1], 3), "a2a_out_ms": round(ms[6], 3),
+            "dense_ms": round(ms[2], 3), "search_overhead_ms": round(ms[3] + ms[4], 3),
+            "kept_density": round(work[1].item() / (H * hp.nb * hp.nb), 4),
+            "gpu_launches": hp.kernels_per_run() * K, "clocks": clocks,
+            "note": "times are max over ranks per phase; value uses the max-over-ranks K4 time",
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def run_reference(args):
@@ -393,6 +486,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.ulysses:
+        run_ulysses(args)
     else:
         run_ours(args)
 

@@ -46,9 +46,10 @@ def lpt_assign(costs, world):
     return [sorted(x) for x in out]
 
 
-def ulysses_in(x_local, group=None, heads_per_rank=None):
+def ulysses_in(x_local, group=None, sizes=None):
     """Sequence-sharded [N_p, H, d] (this rank's token chunk, all heads) -> head-sharded
     [N, Hp, d] (all tokens, this rank's contiguous head group).  H must divide by the world size.
+    sizes: every rank's token count (seq_splits); gathered with one small all_gather if None.
     Returns a contiguous tensor; view it as [1, Hp, N, d] with `as_bhnd` for the kernels."""
     world = dist.get_world_size(group)
     Np, H, d = x_local.shape
@@ -57,10 +58,10 @@ def ulysses_in(x_local, group=None, heads_per_rank=None):
     Hp = H // world
     # send chunk r = heads [r*Hp, (r+1)*Hp) of my tokens: [world, Np, Hp, d] contiguous
     send = x_local.view(Np, world, Hp, d).permute(1, 0, 2, 3).contiguous()
-    sizes = [0] * world
-    all_np = [torch.zeros(1, dtype=torch.int64, device=x_local.device) for _ in range(world)]
-    dist.all_gather(all_np, torch.tensor([Np], dtype=torch.int64, device=x_local.device), group=group)
-    sizes = [int(t.item()) for t in all_np]
+    if sizes is None:
+        all_np = [torch.zeros(1, dtype=torch.int64, device=x_local.device) for _ in range(world)]
+        dist.all_gather(all_np, torch.tensor([Np], dtype=torch.int64, device=x_local.device), group=group)
+        sizes = [int(t.item()) for t in all_np]
     N = sum(sizes)
     recv = torch.empty(N, Hp, d, dtype=x_local.dtype, device=x_local.device)
     dist.all_to_all_single(recv.view(-1), send.view(-1),

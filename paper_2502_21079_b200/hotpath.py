@@ -5,7 +5,8 @@
 This is the search step t_w of the schedule (Alg. 1) followed by the
 block-sparse forward every later step runs (PAPER.md:402-403).  Buffers are allocated once;
 `run()` accepts device tensors or (pinned) host tensors, in which case it stages them to the
-device on the same stream.  Everything runs through the C ABI; nothing here computes.
+device on the same stream; `run_sparse_host()` is a sparse step end to end from host memory.
+Everything runs through the C ABI; nothing here computes.
 """
 
 import torch
@@ -16,19 +17,26 @@ from . import _lib as L
 class HotPath:
     def __init__(self, batch, heads, seq_len, head_dim, block_size, n_text, text_first=False,
                  mode=L.SELECT_RECALL, targets=0.9, flags=L.FLAG_TEXT_SINK, tier_tau=0.8,
-                 softmax_scale=0.0, device="cuda"):
+                 softmax_scale=0.0, device="cuda", token_major=False):
+        """token_major: Q/K/V/O stored [B, N, H, d] (the layout a Ulysses exchange delivers) and
+        viewed as [B, H, N, d]; the kernels read it through the descriptor strides."""
         self.shape = (batch, heads, seq_len, head_dim)
+        self.token_major = token_major
         self.kw = dict(block_size=block_size, n_text=n_text, text_first=text_first, softmax_scale=softmax_scale)
         self.mode, self.flags, self.tier_tau = mode, flags, tier_tau
         self.targets = [float(targets)] * heads if isinstance(targets, (int, float)) else [float(t) for t in targets]
         dev = torch.device(device)
         self.device = dev
         e = lambda *s, dt=torch.bfloat16: torch.empty(*s, dtype=dt, device=dev)  # noqa: E731
-        self.q, self.k, self.v = e(*self.shape), e(*self.shape), e(*self.shape)
+        if token_major:
+            act = lambda: e(batch, seq_len, heads, head_dim).transpose(1, 2)  # noqa: E731
+        else:
+            act = lambda: e(*self.shape)  # noqa: E731
+        self.q, self.k, self.v = act(), act(), act()
         self.desc = L.make_desc(self.q, block_size, n_text, text_first, softmax_scale)
         self.nb = L.num_blocks(self.desc)
-        self.o_dense = e(*self.shape)
-        self.o_sparse = e(*self.shape)
+        self.o_dense = act()
+        self.o_sparse = act()
         self.lse = e(batch, heads, seq_len, dt=torch.float32)
         self.mass = e(batch, heads, self.nb, self.nb, dt=torch.float32)
         rows = batch * heads * self.nb
@@ -65,3 +73,45 @@ class HotPath:
     # K4 3 (stream + order + attention)
     def kernels_per_run(self):
         return 9 + (2 if self.flags & L.FLAG_HEAD_TIERS else 0)
+
+    def run_sparse_host(self, q_host, k_host, v_host, o_host, groups=4):
+        """A sparse denoising step end to end from host memory (the steps between
+        key steps only run the block-sparse forward on the cached index lists): per head group, the
+        H2D copy of Q,K,V on a copy stream overlaps K4 of the previous group on the current stream,
+        and O goes back per group.  q/k/v/o_host: pinned [B, H, N, d] host tensors.  Uses the CSR
+        of the last run() (the cache).  Everything on the device path is the C-ABI's K4."""
+        B, H, N, d = self.shape
+        if B != 1:
+            raise ValueError("run_sparse_host stages head groups of batch 1")
+        cur = torch.cuda.current_stream(self.device)
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream(self.device)
+            self._out_stream = torch.cuda.Stream(self.device)
+        cs, os_ = self._copy_stream, self._out_stream
+        cs.wait_stream(cur)
+        bounds = [H * g // groups for g in range(groups + 1)]
+        done_in, done_k4 = [], []
+        for g in range(groups):
+            h0, h1 = bounds[g], bounds[g + 1]
+            with torch.cuda.stream(cs):
+                for dev, host in ((self.q, q_host), (self.k, k_host), (self.v, v_host)):
+                    dev[:, h0:h1].copy_(host[:, h0:h1], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(cs)
+            done_in.append(e)
+        for g in range(groups):
+            h0, h1 = bounds[g], bounds[g + 1]
+            cur.wait_event(done_in[g])
+            rp = self.csr.row_ptr[h0 * self.nb: h1 * self.nb + 1]
+            L.block_sparse_attn(self.q[:, h0:h1], self.k[:, h0:h1], self.v[:, h0:h1], rp, self.csr.col_idx,
+                                o=self.o_sparse[:, h0:h1], workspace=self.ws, **self.kw)
+            e = torch.cuda.Event()
+            e.record(cur)
+            done_k4.append(e)
+        for g in range(groups):
+            h0, h1 = bounds[g], bounds[g + 1]
+            os_.wait_event(done_k4[g])
+            with torch.cuda.stream(os_):
+                o_host[:, h0:h1].copy_(self.o_sparse[:, h0:h1], non_blocking=True)
+        cur.wait_stream(os_)
+        return o_host

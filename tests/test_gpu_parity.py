@@ -195,3 +195,18 @@ def test_end_to_end_tiny(ada):
             gk = [rows[h * nb + p] for p in range(nb)]
             so, _ = oracle.masked_attention(qq, kk, vv, blocks, gk, scale)
             compare_out(o_s[0, h], so, what=f"{name} sparse h{h}")
+
+
+def test_run_sparse_host_matches_device(ada):
+    """HotPath.run_sparse_host (H2D per head group, K4 on the cached CSR, D2H) == the device K4."""
+    from paper_2502_21079_b200.hotpath import HotPath
+    lay = _lay("tiny", dict(heads=5, head_dim=128, block=128, f=5, h=9, w=11, n_text=37))
+    q, k, v = _qkv(lay)
+    hp = HotPath(1, lay.heads, lay.n, lay.head_dim, lay.block, lay.n_text, lay.text_first, targets=0.9)
+    hp.run(q, k, v)
+    ref = hp.o_sparse.clone()
+    qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
+    oh = torch.empty_like(qh).pin_memory()
+    hp.run_sparse_host(qh, kh, vh, oh, groups=3)
+    torch.cuda.synchronize()
+    assert torch.equal(oh, ref.cpu())
