@@ -6,11 +6,11 @@
 // 128-row q tiles of one head (q-blocks 2p,2p+1 at B=128; 4p..4p+3 at B=64), the kv stream is
 // every kv tile of the head (one block at B=128, two at B=64).  S tiles are double-buffered
 // per q tile in TMEM (4 x 128 columns), so the tensor core runs ahead of the exp work.
-// Exp-role threads own one row: x = fma(S, scale*log2e, -lse*log2e), p = 2^x (MUFU.EX2, one
-// pair in four on the FMA pipe), fp32 partial sums per kv block, a warp-shuffle sum over the
-// warp's 32 rows into shared memory, and every kChunk kv tiles one fixed-order fp64 sum over the
-// 4 warps of the q tile gives one fp32 mass per (q-block, kv-block) -- no per-tile barrier.
-// S is never written to memory.
+// Exp-role warps: two per TMEM lane quarter, each on one 64-column half of the S row (one kv block
+// at B=64, one half block at B=128): x = fma(S, scale*log2e, -lse*log2e), p = 2^x (MUFU.EX2, one
+// pair in 8 on the FMA pipe), fp32 partial sums, a warp-shuffle sum over the warp's 32 rows into
+// shared memory, and every kChunk kv tiles one fixed-order fp64 sum over the warps of the q tile
+// gives one fp32 mass per (q-block, kv-block) -- no per-tile barrier.  S never touches memory.
 #include "attn.cuh"
 #include "common.cuh"
 
@@ -18,9 +18,13 @@ namespace adaspa {
 
 namespace {
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 640;
 
 constexpr int kChunk = 256;  // kv tiles per flush of the per-warp partial masses
+#ifndef ADASPA_SEARCH_POLY_MOD
+#define ADASPA_SEARCH_POLY_MOD 8
+#endif
+constexpr int kSearchPolyMod = ADASPA_SEARCH_POLY_MOD;  // one pair in this many on the FMA-pipe polynomial
 
 template <int D>
 struct SSmem {
@@ -28,7 +32,7 @@ struct SSmem {
   static constexpr int kNS = (D == 128) ? 4 : 8;
   static constexpr int kQ = 0;
   static constexpr int kK = 2 * kTile;
-  static constexpr int kPart = kK + kNS * kTile;                  // float [2 tiles][4 warps][kChunk][2]
+  static constexpr int kPart = kK + kNS * kTile;                  // float [2 tiles][2 halves][4 warps][kChunk]
   static constexpr int kBar = kPart + 2 * 4 * kChunk * 2 * 4;
   static constexpr int kBytes = kBar + 1024 + 1024;
 };
@@ -101,8 +105,9 @@ __device__ __forceinline__ void kv_tile(const SearchParams& p, bool two, int j, 
 
 // Sum of 2^x over 64 consecutive columns held in s[0..63] (fp32 bits), x = S*scale*log2e - lse*log2e
 // (reading R4); columns at or beyond `lim` are excluded.  The argument is one FFMA2 per pair; one
-// pair in four goes through the degree-5 polynomial on the FMA pipe (relative error 2.3e-7, the
-// same class as ex2.approx's 2^-22), the rest through MUFU.EX2; 4 packed partial sums, then a tree.
+// pair in kSearchPolyMod goes through the degree-5 polynomial on the FMA pipe (relative error 2.3e-7,
+// the same class as ex2.approx's 2^-22), the rest through MUFU.EX2; 4 packed partial sums, then a
+// tree.  (Measured on HYV-110K / CogX-45K: 1 in 8 is best; 1 in 4 or 3 loses to the FMA pipe.)
 template <bool FULL>
 __device__ __forceinline__ float half_mass(const uint32_t* s, float2 sl2, float2 nl, int lim) {
   float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -110,7 +115,7 @@ __device__ __forceinline__ float half_mass(const uint32_t* s, float2 sl2, float2
   for (int i = 0; i < 32; ++i) {
     const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sl2, nl);
     float2 e;
-    if ((i & 3) == 3) {
+    if (kSearchPolyMod > 0 && (i % (kSearchPolyMod > 0 ? kSearchPolyMod : 1)) == kSearchPolyMod - 1) {
       e.x = exp2_poly<5>(x.x);
       e.y = exp2_poly<5>(x.y);
     } else {
@@ -155,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = 0; t < 2; ++t)
       for (int b = 0; b < 2; ++b) {
         mbar_init(&bars->s_full[t][b], 1);
-        mbar_init(&bars->s_empty[t][b], 4);
+        mbar_init(&bars->s_empty[t][b], 8);
       }
     fence_mbar_init();
     tma_prefetch_desc(&tq);
@@ -172,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ntiles = p.kv_tiles;
 
   if (warp < 4) {
-  regs_dec<96>();
+  regs_dec<64>();  // pool = 640 x 96 at launch: 64*128 + 104*512 = 61440
   if (warp == 0) {
     if (lane == 0) {
       int slot = 0;
@@ -247,17 +252,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   } else {
-    regs_inc<200>();
+    regs_inc<104>();
     // ============================================================ exp / block-sum warps
-    const int t = (warp - 4) >> 2;
+    // warps 4..19: sw = warp - 4, q tile t = sw >> 3, column half hc = (sw >> 2) & 1 (= kv half:
+    // kv block kb0 / kb1 at B=64, the two halves of one block at B=128), TMEM lane quarter wq.
+    // Two warps per row, each on its own 64 columns: 2 warps per SMSP per q tile, no exchange.
+    const int sw = warp - 4;
+    const int t = sw >> 3;
+    const int hc = (sw >> 2) & 1;
     const int wq = warp & 3;
     const int row = wq * 32 + lane;
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
     const float2 sl2v = make_float2(p.scale_log2, p.scale_log2);
     uint32_t sfph[2] = {0u, 0u};
     const int nb = p.grid.nb;
-    float* my_part = part + (t * 4 + wq) * kChunk * 2;   // this warp's [kChunk][2] partial masses
-    const float* grp_part = part + t * 4 * kChunk * 2;  // the 4 warps of this q tile
+    float* my_part = part + ((t * 2 + hc) * 4 + wq) * kChunk;   // this warp's [kChunk] partial masses
+    const float* grp_part = part + t * 8 * kChunk;             // [hc][wq][kChunk] of this q tile
     for (int item = blockIdx.x; item < p.num_items; item += gridDim.x) {
       QTiles q;
       decode_search_item(p, TWO, item, q);
@@ -283,51 +293,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&bars->s_full[t][buf], sfph[buf]);
           sfph[buf] ^= 1;
           tc_fence_after();
-          uint32_t s[128];
-          const uint32_t sa = tmem + lane_base + t * 256 + buf * 128;
+          uint32_t s[64];
+          const uint32_t sa = tmem + lane_base + t * 256 + buf * 128 + hc * 64;
           tmem_ld32(sa + 0, s);
           tmem_ld32(sa + 32, s + 32);
-          tmem_ld32(sa + 64, s + 64);
-          tmem_ld32(sa + 96, s + 96);
           tmem_ld_wait32(s);
           reg_fence32(s + 32);
-          reg_fence32(s + 64);
-          reg_fence32(s + 96);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars->s_empty[t][buf]);
-          // column limits of the two 64-column halves (kv blocks kb0 / kb1 at B=64)
-          const int lim_a = TWO ? l0 : (l0 < 64 ? l0 : 64);
-          const int lim_b = TWO ? l1 : l0 - 64;
-          float ma, mb;
-          if (lim_a >= 64 && lim_b >= 64) {
-            ma = half_mass<true>(s, sl2v, nlv, 64);
-            mb = half_mass<true>(s + 64, sl2v, nlv, 64);
-          } else {
-            ma = half_mass<false>(s, sl2v, nlv, lim_a);
-            mb = lim_b > 0 ? half_mass<false>(s + 64, sl2v, nlv, lim_b) : 0.0f;
-          }
-          if (!rvalid) {
-            ma = 0.0f;
-            mb = 0.0f;
-          }
-          // warp sum of (ma, mb): after the first exchange lanes 0-15 carry ma, 16-31 carry mb
-          const bool hi = lane & 16;
-          float v = hi ? mb : ma;
-          v += __shfl_xor_sync(0xffffffffu, hi ? ma : mb, 16);
+          // valid columns of my half (kv block kb0 / kb1 at B=64; the two halves of kb0 at B=128)
+          const int lim = TWO ? (hc == 0 ? l0 : l1) : (hc == 0 ? (l0 < 64 ? l0 : 64) : l0 - 64);
+          float mh;
+          if (lim >= 64) mh = half_mass<true>(s, sl2v, nlv, 64);
+          else mh = lim > 0 ? half_mass<false>(s, sl2v, nlv, lim) : 0.0f;
+          if (!rvalid) mh = 0.0f;
 #pragma unroll
-          for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          if ((lane & 15) == 0) my_part[(j - j0) * 2 + (lane >> 4)] = v;
+          for (int o = 16; o > 0; o >>= 1) mh += __shfl_xor_sync(0xffffffffu, mh, o);
+          if (lane == 0) my_part[j - j0] = mh;
         }
-        // flush the chunk: one fixed-order fp64 sum over the 4 warps per (q-block, kv-block)
-        named_bar_sync(1 + t, 128);
-        for (int jj = row; jj < j1 - j0; jj += 128) {
+        // flush the chunk: one fixed-order fp64 sum per (q-block, kv-block)
+        named_bar_sync(1 + t, 256);
+        for (int jj = sw * 32 + lane - t * 256; jj < j1 - j0; jj += 256) {
           const int j = j0 + jj;
           if (!TWO) {
             double m = 0.0;
 #pragma unroll
-            for (int w = 0; w < 4; ++w)
-              m += (double)grp_part[(w * kChunk + jj) * 2] + (double)grp_part[(w * kChunk + jj) * 2 + 1];
+            for (int w = 0; w < 8; ++w) m += (double)grp_part[w * kChunk + jj];
             mout[static_cast<int64_t>(q.qb0[t]) * nb + j] = static_cast<float>(m);
           } else {
 #pragma unroll
@@ -338,14 +330,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int hf = 0; hf < 2; ++hf) {
                 const int kb = 2 * j + hf;
                 if (kb >= nb) continue;
-                const double m = (double)grp_part[((2 * qh) * kChunk + jj) * 2 + hf] +
-                                 (double)grp_part[((2 * qh + 1) * kChunk + jj) * 2 + hf];
+                const double m = (double)grp_part[(hf * 4 + 2 * qh) * kChunk + jj] +
+                                 (double)grp_part[(hf * 4 + 2 * qh + 1) * kChunk + jj];
                 mout[static_cast<int64_t>(qb) * nb + kb] = static_cast<float>(m);
               }
             }
           }
         }
-        named_bar_sync(1 + t, 128);
+        named_bar_sync(1 + t, 256);
       }
     }
   }
