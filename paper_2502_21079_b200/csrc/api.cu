@@ -102,13 +102,16 @@ adaspa_status check_ptr16(const void* p, const char* name) {
   return ADASPA_OK;
 }
 
-adaspa_status make_map(CUtensorMap* map, const void* base, const adaspa_attn_desc* d, const char* name) {
+// Box = 64 columns (128 B, the swizzle span) x box_rows rows: 128-row boxes fetch a whole 128-row tile
+// chunk with one TMA instruction (B = 128, dense); B = 64 tiles are two independent 64-row blocks.
+adaspa_status make_map(CUtensorMap* map, const void* base, const adaspa_attn_desc* d, const char* name,
+                       int box_rows) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(ADASPA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
   cuuint64_t dims[4] = {(cuuint64_t)d->head_dim, (cuuint64_t)d->seq_len, (cuuint64_t)d->heads,
                         (cuuint64_t)d->batch};
   cuuint64_t strides[3] = {(cuuint64_t)d->stride_n * 2, (cuuint64_t)d->stride_h * 2, (cuuint64_t)d->stride_b * 2};
-  cuuint32_t box[4] = {64, 64, 1, 1};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -193,7 +196,8 @@ adaspa_status adaspa_dense_attn_lse(const adaspa_attn_desc* desc, const void* q,
       (s = check_ptr16(o, "o")))
     return s;
   CUtensorMap tq, tk, tv;
-  if ((s = make_map(&tq, q, desc, "q")) || (s = make_map(&tk, k, desc, "k")) || (s = make_map(&tv, v, desc, "v")))
+  if ((s = make_map(&tq, q, desc, "q", 128)) || (s = make_map(&tk, k, desc, "k", 128)) ||
+      (s = make_map(&tv, v, desc, "v", 128)))
     return s;
   AttnParams p{};
   p.B = desc->batch;
@@ -222,7 +226,8 @@ adaspa_status adaspa_lse_cached_search(const adaspa_attn_desc* desc, const void*
   if (reinterpret_cast<uintptr_t>(lse) % 4 || reinterpret_cast<uintptr_t>(block_mass) % 4)
     return fail(ADASPA_ERR_INVALID_ARG, "lse / block_mass misaligned");
   CUtensorMap tq, tk;
-  if ((s = make_map(&tq, q, desc, "q")) || (s = make_map(&tk, k, desc, "k"))) return s;
+  const int rows_s = desc->block_size == 64 ? 64 : 128;
+  if ((s = make_map(&tq, q, desc, "q", rows_s)) || (s = make_map(&tk, k, desc, "k", rows_s))) return s;
   SearchParams p{};
   p.B = desc->batch;
   p.H = desc->heads;
@@ -369,7 +374,9 @@ adaspa_status adaspa_block_sparse_attn(const adaspa_attn_desc* desc, const void*
   if (!workspace || workspace_bytes < w.bytes)
     return fail(ADASPA_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", workspace_bytes, w.bytes);
   CUtensorMap tq, tk, tv;
-  if ((s = make_map(&tq, q, desc, "q")) || (s = make_map(&tk, k, desc, "k")) || (s = make_map(&tv, v, desc, "v")))
+  const int rows_s = desc->block_size == 64 ? 64 : 128;
+  if ((s = make_map(&tq, q, desc, "q", rows_s)) || (s = make_map(&tk, k, desc, "k", rows_s)) ||
+      (s = make_map(&tv, v, desc, "v", rows_s)))
     return s;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   const bool two = desc->block_size == 64;

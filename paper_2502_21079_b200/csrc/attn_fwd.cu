@@ -31,7 +31,7 @@ namespace adaspa {
 // Diagnostic build only (-DADASPA_TRACE): per-tile clock64 stamps of CTA 0 -- softmax warp 4
 // (q tile 0, column half 0) events 0..3 and the MMA issuer's events -- read back through
 // adaspa_debug_trace().  The product library is built without it.
-__device__ unsigned long long g_trace[2][4096];
+__device__ unsigned long long g_trace[4][4096];
 __device__ int g_trace_n[2];
 #define ADASPA_TRACE_EV(k)                                                                    \
   do {                                                                                        \
@@ -40,10 +40,18 @@ __device__ int g_trace_n[2];
   } while (0)
 #define ADASPA_TRACE_MMA(k)                                                                   \
   do {                                                                                        \
-    if (blockIdx.x == 0 && tr_n < 1000) g_trace[1][tr_n * 4 + (k)] = clock64();               \
-    if ((k) == 3) ++tr_n;                                                                     \
+    if (blockIdx.x == 0 && tr_n < 1000) g_trace[1 + ((k) >> 2)][tr_n * 4 + ((k) & 3)] = clock64(); \
+    if ((k) == 5) ++tr_n;                                                                     \
+  } while (0)
+#define ADASPA_TRACE_TMA(k)                                                                   \
+  do {                                                                                        \
+    if (blockIdx.x == 0 && tp_n < 1000) g_trace[3][tp_n * 4 + (k)] = clock64();               \
+    if ((k) == 3) ++tp_n;                                                                     \
   } while (0)
 #else
+#define ADASPA_TRACE_TMA(k) \
+  do {                      \
+  } while (0)
 #define ADASPA_TRACE_EV(k) \
   do {                     \
   } while (0)
@@ -63,6 +71,9 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #endif
 #ifndef ADASPA_EXP_PACKED
 #define ADASPA_EXP_PACKED 1
+#endif
+#ifndef ADASPA_ABLATE
+#define ADASPA_ABLATE 0  // diagnostic builds only: 1 = skip the P store, 2 = skip the max exchange, 3 = no MUFU
 #endif
 constexpr int kExpPolyMod = ADASPA_EXP_POLY_MOD;  // one pair in kExpPolyMod on the FMA-pipe polynomial (0: none)
 constexpr bool kExpPacked = ADASPA_EXP_PACKED;   // FFMA2/FADD2 for the argument and the row sum
@@ -90,18 +101,19 @@ struct ItemInfo {
 template <int D>
 struct Smem {
   static constexpr int kTile = 128 * D * 2;  // one 128-row tile of d bf16 columns
-  static constexpr int kNS = (D == 128) ? 4 : 10;
+  // ADASPA_ABLATE 5 (diagnostic): one shared Q tile, 5 K/V slots -- pipeline depth experiment
+  static constexpr int kNS = (D == 128) ? (ADASPA_ABLATE == 5 ? 5 : 4) : 10;
   static constexpr int kQ = 0;
-  static constexpr int kKV = 2 * kTile;
+  static constexpr int kKV = (ADASPA_ABLATE == 5 ? 1 : 2) * kTile;
   static constexpr int kBar = kKV + kNS * kTile;
   static constexpr int kBytes = kBar + 6144 + 1024;  // barriers/meta/exchange + alignment slack
 };
 
 struct Bars {
-  uint64_t kv_full[10], kv_empty[10];
+  uint64_t kv_full[12], kv_empty[12];
   uint64_t q_full, q_empty;
   uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
-  SlotMeta meta[10];
+  SlotMeta meta[12];
   TileInfo info[2][2];
   ItemInfo qitem;
   uint32_t tmem_base;
@@ -206,6 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int slot = 0;
       uint32_t ph = 0, qph = 0;
       const uint64_t pol_kv = l2_policy_evict_last();
+      int tp_n = 0;
+      (void)tp_n;
       const uint64_t pol_q = l2_policy_evict_first();
       for (int it_n = 0;; ++it_n) {
         int item;
@@ -218,15 +232,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bars->q_empty, qph ^ 1);
         qph ^= 1;
         bars->qitem = it;
-        const uint32_t qbytes = (it.exists[0] ? TILE : 0) + (it.exists[1] ? TILE : 0);
+        const uint32_t qbytes = ADASPA_ABLATE == 5 ? TILE : (it.exists[0] ? TILE : 0) + (it.exists[1] ? TILE : 0);
         mbar_arrive_expect_tx(&bars->q_full, qbytes);
         for (int t = 0; t < 2; ++t) {
           if (!it.exists[t]) continue;
+          if (ADASPA_ABLATE == 5 && t == 1) continue;
           const int r1 = TWO ? it.start1[t] : it.start0[t] + 64;
           for (int c = 0; c < CH; ++c) {
             uint8_t* dst = sQ + t * TILE + c * CHUNK;
             tma_load_4d_hint(&tq, &bars->q_full, dst, c * 64, it.start0[t], it.h, it.b, pol_q);
-            tma_load_4d_hint(&tq, &bars->q_full, dst + CHUNK / 2, c * 64, r1, it.h, it.b, pol_q);
+            if (TWO) tma_load_4d_hint(&tq, &bars->q_full, dst + CHUNK / 2, c * 64, r1, it.h, it.b, pol_q);  // B=64: second block; else one 128-row box
           }
         }
         const int n_ent = SPARSE ? __ldg(p.stream_len + id) : (p.N + 127) / 128;
@@ -256,22 +271,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             mask = dense_mask;
           }
           // K
+          ADASPA_TRACE_TMA(0);
           mbar_wait(&bars->kv_empty[slot], ph ^ 1);
+          ADASPA_TRACE_TMA(1);
           bars->meta[slot] = SlotMeta{kNormal, static_cast<int>(mask), l0, l1};
           mbar_arrive_expect_tx(&bars->kv_full[slot], TILE);
           for (int c = 0; c < CH; ++c) {
             uint8_t* dst = sKV + slot * TILE + c * CHUNK;
             tma_load_4d_hint(&tk, &bars->kv_full[slot], dst, c * 64, s0, it.h, it.b, pol_kv);
-            tma_load_4d_hint(&tk, &bars->kv_full[slot], dst + CHUNK / 2, c * 64, s1, it.h, it.b, pol_kv);
+            if (TWO) tma_load_4d_hint(&tk, &bars->kv_full[slot], dst + CHUNK / 2, c * 64, s1, it.h, it.b, pol_kv);  // B=64: second block; else one 128-row box
           }
           if (++slot == NS) { slot = 0; ph ^= 1; }
           // V
+          ADASPA_TRACE_TMA(2);
           mbar_wait(&bars->kv_empty[slot], ph ^ 1);
+          ADASPA_TRACE_TMA(3);
           mbar_arrive_expect_tx(&bars->kv_full[slot], TILE);
           for (int c = 0; c < CH; ++c) {
             uint8_t* dst = sKV + slot * TILE + c * CHUNK;
             tma_load_4d_hint(&tv, &bars->kv_full[slot], dst, c * 64, s0, it.h, it.b, pol_kv);
-            tma_load_4d_hint(&tv, &bars->kv_full[slot], dst + CHUNK / 2, c * 64, s1, it.h, it.b, pol_kv);
+            if (TWO) tma_load_4d_hint(&tv, &bars->kv_full[slot], dst + CHUNK / 2, c * 64, s1, it.h, it.b, pol_kv);  // B=64: second block; else one 128-row box
           }
           if (++slot == NS) { slot = 0; ph ^= 1; }
         }
@@ -303,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * CHUNK + (kk & 3) * 32;
-          const uint64_t a = desc_sw128(sq_addr + t * TILE + off, 16, 1024);
+          const uint64_t a = desc_sw128(sq_addr + (ADASPA_ABLATE == 5 ? 0 : t) * TILE + off, 16, 1024);
           const uint64_t b = desc_sw128(skv_addr + kslot * TILE + off, 16, 1024);
           mma_ss(tmem + s_col(t), a, b, kIdescQK, kk > 0 ? 1u : 0u);
         }
@@ -391,6 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++slot == NS) { slot = 0; ph ^= 1; }
           if (pvslot >= 0) {
             mbar_wait(&bars->kv_full[pvslot], pvph);
+            ADASPA_TRACE_MMA(4);
             tc_fence_after();
           }
 #pragma unroll
@@ -439,6 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           pvslot = vslot;
           pvph = vph;
           mbar_wait(&bars->kv_full[slot], ph);
+          ADASPA_TRACE_MMA(5);
           tc_fence_after();
           mt = bars->meta[slot];
         }
@@ -530,6 +551,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         ntile = 0;
         continue;
       }
+      if (ADASPA_ABLATE == 4 || ADASPA_ABLATE == 5) {  // diagnostic: no softmax (MMA/TMA pipeline alone)
+        ADASPA_TRACE_EV(1);
+        ADASPA_TRACE_EV(2);
+        tc_fence_before();
+        __syncwarp();
+        ADASPA_TRACE_EV(3);
+        if (lane == 0) mbar_arrive(&bars->p_full[t]);
+        ++ntile;
+        continue;
+      }
       // my 64 columns [64hc, 64hc+64): valid below `lim` (relative)
       const int lim = hc == 0 ? inf.lim[hq * 2 + 0] : inf.lim[hq * 2 + 1] - 64;
       uint32_t s[64];
@@ -553,10 +584,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float lmx = fmax3(mx4[0], mx4[1], fmaxf(mx4[2], mx4[3]));
       // the partner warp holds the other 64 columns of the same rows; the barrier also orders
       // both halves' TMEM loads of S before either overwrites S columns with P
-      xm[hc * 128 + row] = lmx;
-      named_bar_sync(1 + t, 256);
+      float mx = lmx;
+      if (ADASPA_ABLATE != 2) {  // 2: diagnostic, each half uses its own max (wrong O; timing only)
+        xm[hc * 128 + row] = lmx;
+        named_bar_sync(1 + t, 256);
+        mx = fmaxf(lmx, xm[(1 - hc) * 128 + row]);
+      }
       ADASPA_TRACE_EV(2);
-      const float mx = fmaxf(lmx, xm[(1 - hc) * 128 + row]);
       const float mx2 = mx * sl2;
       const float m_new = fmaxf(m_used, mx2);
       const bool grow = m_new > m_used + kRescaleThreshold;  // also true when m_used == -inf
@@ -603,6 +637,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           float2 pv;
           if (kExpPolyMod > 0 && (i % (kExpPolyMod > 0 ? kExpPolyMod : 1)) == kExpPolyMod - 1) {
             pv = exp2_poly4x2(x, poly);
+          } else if (ADASPA_ABLATE == 3) {  // diagnostic: no MUFU (wrong P; timing only)
+            pv.x = x.x * 0.5f + 1.0f;
+            pv.y = x.y * 0.5f + 1.0f;
           } else {
             pv.x = ex2_approx(x.x);
             pv.y = ex2_approx(x.y);
@@ -615,7 +652,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           pk[i] = pack_bf16x2(pv.x, pv.y);
         }
-        tmem_st16(s_addr + hc * 32 + c * 16, pk);
+        if (ADASPA_ABLATE != 1) tmem_st16(s_addr + hc * 32 + c * 16, pk);  // 1: diagnostic, no P store
+        else if (pk[0] == 0x7fffffffu && pk[15] == 0x1u) l_sum += 1.0f;  // keep pk live
       }
       const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
       const float2 a = fadd2(a01, a23);
@@ -740,7 +778,7 @@ __global__ void __launch_bounds__(256) sparse_order_kernel(SparsePrepParams p) {
 
 #ifdef ADASPA_TRACE
 extern "C" int adaspa_debug_trace(unsigned long long* host, int n) {
-  if (cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * (n < 8192 ? n : 8192)) != cudaSuccess) return -1;
+  if (cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * (n < 16384 ? n : 16384)) != cudaSuccess) return -1;
   return 0;
 }
 #endif

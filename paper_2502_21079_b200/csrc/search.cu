@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < CH; ++c) {
             uint8_t* dst = sQ + t * TILE + c * CHUNK;
             tma_load_4d_hint(&tq, &bars->q_full, dst, c * 64, q.start0[t], q.h, q.b, pol_q);
-            tma_load_4d_hint(&tq, &bars->q_full, dst + CHUNK / 2, c * 64, r1, q.h, q.b, pol_q);
+            if (TWO) tma_load_4d_hint(&tq, &bars->q_full, dst + CHUNK / 2, c * 64, r1, q.h, q.b, pol_q);  // B=64: second block; else one 128-row box
           }
         }
         for (int j = 0; j < ntiles; ++j) {
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < CH; ++c) {
             uint8_t* dst = sK + slot * TILE + c * CHUNK;
             tma_load_4d_hint(&tk, &bars->kv_full[slot], dst, c * 64, s0, q.h, q.b, pol_k);
-            tma_load_4d_hint(&tk, &bars->kv_full[slot], dst + CHUNK / 2, c * 64, s1, q.h, q.b, pol_k);
+            if (TWO) tma_load_4d_hint(&tk, &bars->kv_full[slot], dst + CHUNK / 2, c * 64, s1, q.h, q.b, pol_k);  // B=64: second block; else one 128-row box
           }
           if (++slot == NS) { slot = 0; ph ^= 1; }
         }
