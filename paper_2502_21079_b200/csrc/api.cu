@@ -5,6 +5,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -144,6 +145,16 @@ SelectWs select_ws_layout(const adaspa_attn_desc* d) {
   return w;
 }
 
+// d = 128 runs on a CTA pair (attn2_fwd.cu) for the dense pass and for the sparse pass at block 128;
+// Opt-in (ADASPA_PAIR=1) until it beats the one-SM kernel of attn_fwd.cu.
+bool use_pair(const adaspa_attn_desc* d, bool sparse) {
+  static const bool enabled = [] {
+    const char* e = getenv("ADASPA_PAIR");
+    return e && e[0] == '1';
+  }();
+  return enabled && d->head_dim == 128 && (!sparse || d->block_size == 128);
+}
+
 struct SparseWs {
   int items_per_bh, num_items, stride;
   size_t queue, len, order, stream, bytes;
@@ -151,8 +162,9 @@ struct SparseWs {
 SparseWs sparse_ws_layout(const adaspa_attn_desc* d) {
   const BlockGrid g = make_grid(d);
   const bool two = d->block_size == 64;
+  const bool quad = use_pair(d, true);
   SparseWs w;
-  w.items_per_bh = two ? (g.nb + 3) / 4 : (g.nb + 1) / 2;
+  w.items_per_bh = (two || quad) ? (g.nb + 3) / 4 : (g.nb + 1) / 2;
   w.num_items = d->batch * d->heads * w.items_per_bh;
   w.stride = two ? (g.nb + 1) / 2 : g.nb;
   size_t off = 0;
@@ -196,7 +208,8 @@ adaspa_status adaspa_dense_attn_lse(const adaspa_attn_desc* desc, const void* q,
       (s = check_ptr16(o, "o")))
     return s;
   CUtensorMap tq, tk, tv;
-  if ((s = make_map(&tq, q, desc, "q", 128)) || (s = make_map(&tk, k, desc, "k", 128)) ||
+  const bool pair = use_pair(desc, false);
+  if ((s = make_map(&tq, q, desc, "q", 128)) || (s = make_map(&tk, k, desc, "k", pair ? 64 : 128)) ||
       (s = make_map(&tv, v, desc, "v", 128)))
     return s;
   AttnParams p{};
@@ -210,9 +223,10 @@ adaspa_status adaspa_dense_attn_lse(const adaspa_attn_desc* desc, const void* q,
   p.sh = desc->stride_h;
   p.sn = desc->stride_n;
   p.lse = lse;
-  p.items_per_bh = (desc->seq_len + 255) / 256;
+  p.items_per_bh = pair ? (desc->seq_len + 511) / 512 : (desc->seq_len + 255) / 256;
   p.num_items = desc->batch * desc->heads * p.items_per_bh;
-  cudaError_t e = launch_attn(tq, tk, tv, p, desc->head_dim, false, false, num_sms(), (cudaStream_t)stream);
+  cudaError_t e = pair ? launch_attn_pair(tq, tk, tv, p, false, num_sms(), (cudaStream_t)stream)
+                       : launch_attn(tq, tk, tv, p, desc->head_dim, false, false, num_sms(), (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "dense_attn_lse launch");
   return ADASPA_OK;
 }
@@ -374,8 +388,9 @@ adaspa_status adaspa_block_sparse_attn(const adaspa_attn_desc* desc, const void*
   if (!workspace || workspace_bytes < w.bytes)
     return fail(ADASPA_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", workspace_bytes, w.bytes);
   CUtensorMap tq, tk, tv;
+  const bool pair = use_pair(desc, true);
   const int rows_s = desc->block_size == 64 ? 64 : 128;
-  if ((s = make_map(&tq, q, desc, "q", rows_s)) || (s = make_map(&tk, k, desc, "k", rows_s)) ||
+  if ((s = make_map(&tq, q, desc, "q", rows_s)) || (s = make_map(&tk, k, desc, "k", pair ? 64 : rows_s)) ||
       (s = make_map(&tv, v, desc, "v", rows_s)))
     return s;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
@@ -388,6 +403,7 @@ adaspa_status adaspa_block_sparse_attn(const adaspa_attn_desc* desc, const void*
   pp.H = desc->heads;
   pp.grid = g;
   pp.two = two ? 1 : 0;
+  pp.quad = pair ? 1 : 0;
   pp.items_per_bh = w.items_per_bh;
   pp.num_items = w.num_items;
   pp.row_ptr = row_ptr;
@@ -415,7 +431,8 @@ adaspa_status adaspa_block_sparse_attn(const adaspa_attn_desc* desc, const void*
   p.stream_len = pp.stream_len;
   p.stream_stride = w.stride;
   p.queue = reinterpret_cast<int*>(ws + w.queue);
-  e = launch_attn(tq, tk, tv, p, desc->head_dim, two, true, num_sms(), st);
+  e = pair ? launch_attn_pair(tq, tk, tv, p, true, num_sms(), st)
+           : launch_attn(tq, tk, tv, p, desc->head_dim, two, true, num_sms(), st);
   if (e != cudaSuccess) return cuda_fail(e, "block_sparse_attn launch");
   return ADASPA_OK;
 }

@@ -18,10 +18,11 @@
 //               PV_0(prev), QK_0(e), PV_1(prev), QK_1(e) -- softmax of one tile overlaps the
 //               MMAs of the other (ping-pong).
 //   warp 2      TMEM allocator (512 columns: S_0 | S_1 | O_0 | O_1).
-//   warps 4-7   softmax for q tile 0, warps 8-11 for q tile 1; thread = one row (TMEM lane).
-//               exp2 domain, conditional rescaling of O (only when the running max grows by
-//               more than 8 in log2 units -- exact, the final normalisation uses the same max),
-//               P written back to TMEM as bf16 over the first 64 columns of S_t.
+//   warps 4-11  softmax for q tile 0, warps 12-19 for q tile 1; each warp owns 16 whole rows
+//               (16-lane TMEM shapes, a thread quad per row: max / sum by quad shuffles, no
+//               exchange between warps).  exp2 domain, conditional rescaling of O (only when the
+//               running max grows by more than 8 in log2 units -- exact, the final normalisation
+//               uses the same max), P written back to TMEM as bf16 over the first 64 columns of S_t.
 #include "attn.cuh"
 #include "common.cuh"
 
@@ -69,14 +70,10 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef ADASPA_EXP_POLY_MOD
 #define ADASPA_EXP_POLY_MOD 0
 #endif
-#ifndef ADASPA_EXP_PACKED
-#define ADASPA_EXP_PACKED 1
-#endif
 #ifndef ADASPA_ABLATE
-#define ADASPA_ABLATE 0  // diagnostic builds only: 1 = skip the P store, 2 = skip the max exchange, 3 = no MUFU
+#define ADASPA_ABLATE 0  // diagnostic builds only: 4 = no softmax, 5 = no softmax + one shared Q tile
 #endif
 constexpr int kExpPolyMod = ADASPA_EXP_POLY_MOD;  // one pair in kExpPolyMod on the FMA-pipe polynomial (0: none)
-constexpr bool kExpPacked = ADASPA_EXP_PACKED;   // FFMA2/FADD2 for the argument and the row sum
 
 enum : int { kNormal = 0, kEnd = 1, kAllEnd = 2 };
 
@@ -117,8 +114,6 @@ struct Bars {
   TileInfo info[2][2];
   ItemInfo qitem;
   uint32_t tmem_base;
-  float xm[2][2 * 128];  // per q tile: row-max of column half 0 | half 1
-  float xl[2][2 * 128];  // per q tile: row-sum of column half 0 | half 1
 };
 
 __device__ __forceinline__ void decode_item(const AttnParams& p, bool sparse, bool two, int id, ItemInfo& it) {
@@ -469,28 +464,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     regs_inc<104>();
     // ============================================================ softmax warps
-    // warps 4..19: sw = warp - 4, q tile t = sw >> 3, column half hc = (sw >> 2) & 1, TMEM lane
-    // quarter wq = warp & 3.  Two warps (one per column half) share each row: 2 warps per SMSP
-    // per q tile, so one warp's dependency stalls are covered by the other's work.
+    // warps 4..19: sw = warp - 4, q tile t = sw >> 3; the warp owns 16 WHOLE rows of the tile: TMEM
+    // lanes [32 wq + 16 hh, +16) with wq = warp & 3 (its lane quarter) and hh = (sw >> 2) & 1.
+    // Through the 16-lane TMEM shapes a thread quad shares a row (thread i: rows r0 = base + i/4 and
+    // r1 = r0 + 8, 32 of the 128 columns each), so the row max and row sum are two quad shuffles and
+    // P overwrites only S columns of the warp's own rows: no shared-memory exchange, no barrier
+    // between warps on the per-tile path.
     const int sw = warp - 4;
     const int t = sw >> 3;
-    const int hc = (sw >> 2) & 1;
+    const int hh = (sw >> 2) & 1;
     const int wq = warp & 3;
-    const int row = wq * 32 + lane;          // row of the q tile (TMEM lane)
-    const int hq = wq >> 1;                  // 64-row half
-    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+    const int hq = wq >> 1;                        // 64-row half of the q tile
+    const int qd = lane & 3;                       // position in the quad
+    const int row0 = wq * 32 + hh * 16 + (lane >> 2);
+    const int row1 = row0 + 8;
+    const uint32_t lane_base = static_cast<uint32_t>(wq * 32 + hh * 16) << 16;
     const uint32_t s_addr = tmem + lane_base + s_col(t);
-    const uint32_t o_addr = tmem + lane_base + o_col(t) + hc * (D / 2);
-    float* xm = bars->xm[t];                 // [2][128] row-max exchange
-    float* xl = bars->xl[t];                 // [2][128] row-sum exchange
+    const uint32_t o_addr = tmem + lane_base + o_col(t);
     const float sl2 = p.scale_log2;
     uint32_t sph = 0, oph = 0;
     int icnt = 0;
-    float m_used = -INFINITY, l_sum = 0.0f;
+    float m_used[2] = {-INFINITY, -INFINITY};
+    float l_sum[2] = {0.0f, 0.0f};  // this thread's share (its 32 columns) of the row sums
     int ntile = 0;
     int tr_k = 0;
     (void)tr_k;
-    const Poly4x2 poly;
+    const Poly3x2 poly;
     for (;;) {
       mbar_wait(&bars->s_full[t], sph);
       sph ^= 1;
@@ -503,51 +502,67 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (kind == kEnd) {
         if (inf.has) {
           const int b = inf.b, h = inf.h;
-          int tok;
-          bool valid;
-          if (!TWO) {
-            tok = inf.start0 + row;
-            valid = row < inf.len0;
-          } else if (row < 64) {
-            tok = inf.start0 + row;
-            valid = row < inf.len0;
-          } else {
-            tok = inf.start1 + row - 64;
-            valid = row - 64 < inf.len1;
+          int tok[2];
+          bool valid[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int row = j ? row1 : row0;
+            if (!TWO) {
+              tok[j] = inf.start0 + row;
+              valid[j] = row < inf.len0;
+            } else if (row < 64) {
+              tok[j] = inf.start0 + row;
+              valid[j] = row < inf.len0;
+            } else {
+              tok[j] = inf.start1 + row - 64;
+              valid[j] = row - 64 < inf.len1;
+            }
           }
-          xl[hc * 128 + row] = l_sum;
-          named_bar_sync(1 + t, 256);
-          const float l_tot = l_sum + xl[(1 - hc) * 128 + row];
+          float l_tot[2], inv[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            float l = l_sum[j];
+            l += __shfl_xor_sync(0xffffffffu, l, 1);
+            l += __shfl_xor_sync(0xffffffffu, l, 2);
+            l_tot[j] = l;
+            inv[j] = l > 0.0f ? 1.0f / l : 0.0f;
+          }
           mbar_wait(&bars->o_full[t], oph);
           oph ^= 1;
           tc_fence_after();
-          const float inv = l_tot > 0.0f ? 1.0f / l_tot : 0.0f;
-          __nv_bfloat16* optr = p.o + b * p.sb + h * p.sh + static_cast<int64_t>(tok) * p.sn + hc * (D / 2);
+          __nv_bfloat16* optr[2];
 #pragma unroll
-          for (int c = 0; c < D / 64; ++c) {
-            uint32_t r[32];
-            tmem_ld32(o_addr + c * 32, r);
-            tmem_ld_wait32(r);
-            uint32_t pk[16];
+          for (int j = 0; j < 2; ++j)
+            optr[j] = p.o + b * p.sb + h * p.sh + static_cast<int64_t>(valid[j] ? tok[j] : 0) * p.sn + 2 * qd;
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]) * inv, __uint_as_float(r[2 * i + 1]) * inv);
-            if (valid) {
-              uint4* dst = reinterpret_cast<uint4*>(optr + c * 32);
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t r[16];
+            tmem_ld_16x256b_x4(o_addr + c * 32, r);
+            tmem_ld_wait16(r);
 #pragma unroll
-              for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            for (int k = 0; k < 4; ++k) {
+              const int col = 32 * c + 8 * k;
+              if (valid[0])
+                *reinterpret_cast<uint32_t*>(optr[0] + col) =
+                    pack_bf16x2(__uint_as_float(r[4 * k]) * inv[0], __uint_as_float(r[4 * k + 1]) * inv[0]);
+              if (valid[1])
+                *reinterpret_cast<uint32_t*>(optr[1] + col) =
+                    pack_bf16x2(__uint_as_float(r[4 * k + 2]) * inv[1], __uint_as_float(r[4 * k + 3]) * inv[1]);
             }
           }
-          if (hc == 0 && valid && p.lse) {
-            const float lv = l_tot > 0.0f ? (m_used + __log2f(l_tot)) * kLn2 : -INFINITY;
-            p.lse[(static_cast<int64_t>(b) * p.H + h) * p.N + tok] = lv;
+          if (qd == 0 && p.lse) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              if (valid[j])
+                p.lse[(static_cast<int64_t>(b) * p.H + h) * p.N + tok[j]] =
+                    l_tot[j] > 0.0f ? (m_used[j] + __log2f(l_tot[j])) * kLn2 : -INFINITY;
           }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars->o_empty[t]);
         }
-        m_used = -INFINITY;
-        l_sum = 0.0f;
+        m_used[0] = m_used[1] = -INFINITY;
+        l_sum[0] = l_sum[1] = 0.0f;
         ntile = 0;
         continue;
       }
@@ -561,103 +576,99 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++ntile;
         continue;
       }
-      // my 64 columns [64hc, 64hc+64): valid below `lim` (relative)
-      const int lim = hc == 0 ? inf.lim[hq * 2 + 0] : inf.lim[hq * 2 + 1] - 64;
+      // valid columns: [0, limA) of kv half 0 and [64, limB) of kv half 1 (absolute, 0..128)
+      const int limA = inf.lim[hq * 2 + 0];
+      const int limB = inf.lim[hq * 2 + 1];
       uint32_t s[64];
-      tmem_ld32(s_addr + hc * 64, s);
-      tmem_ld32(s_addr + hc * 64 + 32, s + 32);
+      tmem_ld_16x256b_x8(s_addr, s);
+      tmem_ld_16x256b_x8(s_addr + 64, s + 32);
       tmem_ld_wait32(s);
       reg_fence32(s + 32);
       ADASPA_TRACE_EV(1);
-      if (lim < 64) {  // partial tile / unneeded half: those columns -> -inf
+      if (limA < 64 || limB < 128) {  // partial tile / unneeded half: those columns -> -inf
 #pragma unroll
-        for (int i = 0; i < 64; ++i) s[i] = i < lim ? s[i] : __float_as_uint(-INFINITY);
-      }
-      float mx4[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) mx4[a] = fmaxf(__uint_as_float(s[a]), __uint_as_float(s[4 + a]));
-#pragma unroll
-      for (int i = 8; i < 64; i += 8) {
-#pragma unroll
-        for (int a = 0; a < 4; ++a) mx4[a] = fmax3(mx4[a], __uint_as_float(s[i + a]), __uint_as_float(s[i + 4 + a]));
-      }
-      const float lmx = fmax3(mx4[0], mx4[1], fmaxf(mx4[2], mx4[3]));
-      // the partner warp holds the other 64 columns of the same rows; the barrier also orders
-      // both halves' TMEM loads of S before either overwrites S columns with P
-      float mx = lmx;
-      if (ADASPA_ABLATE != 2) {  // 2: diagnostic, each half uses its own max (wrong O; timing only)
-        xm[hc * 128 + row] = lmx;
-        named_bar_sync(1 + t, 256);
-        mx = fmaxf(lmx, xm[(1 - hc) * 128 + row]);
-      }
-      ADASPA_TRACE_EV(2);
-      const float mx2 = mx * sl2;
-      const float m_new = fmaxf(m_used, mx2);
-      const bool grow = m_new > m_used + kRescaleThreshold;  // also true when m_used == -inf
-      float alpha = 1.0f;
-      if (grow) {
-        alpha = (m_used == -INFINITY) ? 0.0f : exp2f(m_used - m_new);
-        l_sum *= alpha;
-        m_used = m_new;
-      }
-      const bool rescale_o = grow && alpha != 0.0f && ntile > 0;
-      if (__any_sync(0xffffffffu, rescale_o)) {
-        const float a = rescale_o ? alpha : 1.0f;
-#pragma unroll 1
-        for (int c = 0; c < D / 64; ++c) {
-          uint32_t r[32];
-          tmem_ld32(o_addr + c * 32, r);
-          tmem_ld_wait32(r);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * a);
-          tmem_st32(o_addr + c * 32, r);
+        for (int i = 0; i < 64; ++i) {
+          const int col = 8 * (i >> 2) + 2 * qd + (i & 1);
+          const int lim = col < 64 ? limA : limB;
+          s[i] = col < lim ? s[i] : __float_as_uint(-INFINITY);
         }
       }
-      const float mb = (m_used == -INFINITY) ? 0.0f : m_used;
-      // P = 2^(S*scale*log2e - m): FFMA2 for the argument, MUFU.EX2 for 3 of every 4 pairs and a
-      // packed degree-4 polynomial on the FMA pipe for the 4th (exp offload; it keeps the LSE --
-      // the search's cache -- at MUFU accuracy).  P is packed to bf16 pairs: S column c of this
-      // half lands in P column 32hc + c/2 (the P of a tile occupies S columns [0, 64)).
+      float mxa[2], mxb[2];  // two partial maxima per row
+      mxa[0] = fmaxf(__uint_as_float(s[0]), __uint_as_float(s[1]));
+      mxb[0] = fmaxf(__uint_as_float(s[4]), __uint_as_float(s[5]));
+      mxa[1] = fmaxf(__uint_as_float(s[2]), __uint_as_float(s[3]));
+      mxb[1] = fmaxf(__uint_as_float(s[6]), __uint_as_float(s[7]));
+#pragma unroll
+      for (int k = 2; k < 16; k += 2) {
+        mxa[0] = fmax3(mxa[0], __uint_as_float(s[4 * k]), __uint_as_float(s[4 * k + 1]));
+        mxb[0] = fmax3(mxb[0], __uint_as_float(s[4 * k + 4]), __uint_as_float(s[4 * k + 5]));
+        mxa[1] = fmax3(mxa[1], __uint_as_float(s[4 * k + 2]), __uint_as_float(s[4 * k + 3]));
+        mxb[1] = fmax3(mxb[1], __uint_as_float(s[4 * k + 6]), __uint_as_float(s[4 * k + 7]));
+      }
+      float mb[2];
+      float alpha[2] = {1.0f, 1.0f};
+      bool rescale = false;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        float mx = fmaxf(mxa[j], mxb[j]);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_used[j], mx * sl2);
+        if (m_new > m_used[j] + kRescaleThreshold) {  // also true when m_used == -inf
+          alpha[j] = (m_used[j] == -INFINITY) ? 0.0f : exp2f(m_used[j] - m_new);
+          l_sum[j] *= alpha[j];
+          m_used[j] = m_new;
+          rescale |= alpha[j] != 0.0f && ntile > 0;
+        }
+        mb[j] = (m_used[j] == -INFINITY) ? 0.0f : m_used[j];
+      }
+      ADASPA_TRACE_EV(2);
+      if (__any_sync(0xffffffffu, rescale)) {  // rare: the running max grew by more than 2^8
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[16];
+          tmem_ld_16x256b_x4(o_addr + c * 32, r);
+          tmem_ld_wait16(r);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha[(i >> 1) & 1]);
+          tmem_st_16x256b_x4(o_addr + c * 32, r);
+        }
+      }
+      // P = 2^(S*scale*log2e - m): FFMA2 for the argument, MUFU.EX2 (one pair in kExpPolyMod on a
+      // packed degree-3 polynomial on the FMA pipe, rel. error 1e-4 -- below P's bf16 rounding),
+      // packed to bf16 pairs: S columns 8k + 2qd + {0,1} -> P column 4k + qd (16x128b layout).
       const float2 sl2v = make_float2(sl2, sl2);
-      const float2 nmb = make_float2(-mb, -mb);
+      const float2 nm0 = make_float2(-mb[0], -mb[0]);
+      const float2 nm1 = make_float2(-mb[1], -mb[1]);
       float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t pk[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float s0 = __uint_as_float(s[32 * c + 2 * i]), s1 = __uint_as_float(s[32 * c + 2 * i + 1]);
-          float2 x;
-          if (kExpPacked) {
-            x = ffma2(make_float2(s0, s1), sl2v, nmb);
+        for (int k = 0; k < 8; ++k) {
+          const int i = 32 * c + 4 * k;
+          const float2 x0 = ffma2(make_float2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sl2v, nm0);
+          const float2 x1 = ffma2(make_float2(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])), sl2v, nm1);
+          float2 p0, p1;
+          if (kExpPolyMod > 0 && (k % (kExpPolyMod > 0 ? kExpPolyMod : 1)) == kExpPolyMod - 1) {
+            p0 = exp2_poly3x2(x0, poly);
+            p1 = exp2_poly3x2(x1, poly);
           } else {
-            x.x = fmaf(s0, sl2, -mb);
-            x.y = fmaf(s1, sl2, -mb);
+            p0.x = ex2_approx(x0.x);
+            p0.y = ex2_approx(x0.y);
+            p1.x = ex2_approx(x1.x);
+            p1.y = ex2_approx(x1.y);
           }
-          float2 pv;
-          if (kExpPolyMod > 0 && (i % (kExpPolyMod > 0 ? kExpPolyMod : 1)) == kExpPolyMod - 1) {
-            pv = exp2_poly4x2(x, poly);
-          } else if (ADASPA_ABLATE == 3) {  // diagnostic: no MUFU (wrong P; timing only)
-            pv.x = x.x * 0.5f + 1.0f;
-            pv.y = x.y * 0.5f + 1.0f;
-          } else {
-            pv.x = ex2_approx(x.x);
-            pv.y = ex2_approx(x.y);
-          }
-          if (kExpPacked) {
-            acc[i & 3] = fadd2(acc[i & 3], pv);
-          } else {
-            acc[i & 3].x += pv.x;
-            acc[i & 3].y += pv.y;
-          }
-          pk[i] = pack_bf16x2(pv.x, pv.y);
+          acc[(k & 1) * 2 + 0] = fadd2(acc[(k & 1) * 2 + 0], p0);
+          acc[(k & 1) * 2 + 1] = fadd2(acc[(k & 1) * 2 + 1], p1);
+          pk[2 * k] = pack_bf16x2(p0.x, p0.y);
+          pk[2 * k + 1] = pack_bf16x2(p1.x, p1.y);
         }
-        if (ADASPA_ABLATE != 1) tmem_st16(s_addr + hc * 32 + c * 16, pk);  // 1: diagnostic, no P store
-        else if (pk[0] == 0x7fffffffu && pk[15] == 0x1u) l_sum += 1.0f;  // keep pk live
+        tmem_st_16x128b_x8(s_addr + c * 32, pk);
       }
-      const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
-      const float2 a = fadd2(a01, a23);
-      l_sum += a.x + a.y;
+      const float2 a0 = fadd2(acc[0], acc[2]), a1 = fadd2(acc[1], acc[3]);
+      l_sum[0] += a0.x + a0.y;
+      l_sum[1] += a1.x + a1.y;
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -666,7 +677,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++ntile;
     }
   }
-
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -685,7 +695,7 @@ __global__ void __launch_bounds__(256) sparse_stream_kernel(SparsePrepParams p) 
   const int bh = item / p.items_per_bh;
   const int pi = item - bh * p.items_per_bh;
   const int nb = p.grid.nb;
-  const int nq = p.two ? 4 : 2;
+  const int nq = (p.two || p.quad) ? 4 : 2;
   int rbeg[4], rend[4];
   for (int s = 0; s < 4; ++s) {
     const int qb = nq * pi + s;
@@ -729,7 +739,9 @@ __global__ void __launch_bounds__(256) sparse_stream_kernel(SparsePrepParams p) 
       const int j = w * 32 + lane;
       uint32_t memb = 0;
       for (int s = 0; s < 4; ++s) memb |= ((word[s] >> lane) & 1u) << s;
-      if (!p.two) {
+      if (p.quad) {
+        out[pos] = stream_entry(j, j, memb);  // bit s: q-block 4p + s of the item keeps kv block j
+      } else if (!p.two) {
         const uint32_t mask = ((memb & 1u) ? 0x0Fu : 0u) | ((memb & 2u) ? 0xF0u : 0u);
         out[pos] = stream_entry(j, j, mask);
       } else {

@@ -37,6 +37,8 @@ CASES = [
     ("tiny", dict(f=5, h=9, w=11, n_text=37, head_dim=128, block=128)),      # 495 + 37 tokens, d=128
     ("tiny_tf", dict(f=3, h=10, w=13, n_text=77, head_dim=64, block=128)),   # text first, B=128
     ("tiny", dict(f=4, h=9, w=10, n_text=45, head_dim=128, block=64, heads=3)),
+    # d=128 at block 128 runs on the CTA pair: several 512-row items per head, ragged last item
+    ("tiny_tf", dict(f=6, h=10, w=21, n_text=77, head_dim=128, block=128, heads=3)),  # 77 + 1260 tokens
 ]
 
 
@@ -147,7 +149,7 @@ def _random_csr(H, nb, density, seed):
 
 
 @pytest.mark.parametrize("name,over", CASES)
-@pytest.mark.parametrize("density", [0.3, 1.0])
+@pytest.mark.parametrize("density", [0.05, 0.3, 1.0])
 def test_block_sparse_attn(ada, name, over, density):
     """K4 vs oracle masked attention (c = +inf) on the same CSR."""
     lay = _lay(name, over)
