@@ -145,7 +145,7 @@ SelectWs select_ws_layout(const adaspa_attn_desc* d) {
   return w;
 }
 
-// d = 128 runs on a CTA pair (attn2_fwd.cu) for the dense pass and for the sparse pass at block 128;
+// d = 128 runs on a CTA pair (attn_pair.cu) for the dense pass and for the sparse pass at block 128;
 // Opt-in (ADASPA_PAIR=1) until it beats the one-SM kernel of attn_fwd.cu.
 bool use_pair(const adaspa_attn_desc* d, bool sparse) {
   static const bool enabled = [] {
@@ -162,9 +162,8 @@ struct SparseWs {
 SparseWs sparse_ws_layout(const adaspa_attn_desc* d) {
   const BlockGrid g = make_grid(d);
   const bool two = d->block_size == 64;
-  const bool quad = use_pair(d, true);
   SparseWs w;
-  w.items_per_bh = (two || quad) ? (g.nb + 3) / 4 : (g.nb + 1) / 2;
+  w.items_per_bh = two ? (g.nb + 3) / 4 : (g.nb + 1) / 2;
   w.num_items = d->batch * d->heads * w.items_per_bh;
   w.stride = two ? (g.nb + 1) / 2 : g.nb;
   size_t off = 0;
@@ -223,7 +222,7 @@ adaspa_status adaspa_dense_attn_lse(const adaspa_attn_desc* desc, const void* q,
   p.sh = desc->stride_h;
   p.sn = desc->stride_n;
   p.lse = lse;
-  p.items_per_bh = pair ? (desc->seq_len + 511) / 512 : (desc->seq_len + 255) / 256;
+  p.items_per_bh = (desc->seq_len + 255) / 256;
   p.num_items = desc->batch * desc->heads * p.items_per_bh;
   cudaError_t e = pair ? launch_attn_pair(tq, tk, tv, p, false, num_sms(), (cudaStream_t)stream)
                        : launch_attn(tq, tk, tv, p, desc->head_dim, false, false, num_sms(), (cudaStream_t)stream);
@@ -403,7 +402,6 @@ adaspa_status adaspa_block_sparse_attn(const adaspa_attn_desc* desc, const void*
   pp.H = desc->heads;
   pp.grid = g;
   pp.two = two ? 1 : 0;
-  pp.quad = pair ? 1 : 0;
   pp.items_per_bh = w.items_per_bh;
   pp.num_items = w.num_items;
   pp.row_ptr = row_ptr;

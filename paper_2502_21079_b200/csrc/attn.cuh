@@ -34,7 +34,6 @@ struct SparsePrepParams {
   int B, H;
   BlockGrid grid;
   int two;                   // block 64 (two blocks per 128-row tile)
-  int quad;                  // CTA-pair kernel (block 128): items of four q-blocks, entry mask = 4-bit membership
   int items_per_bh, num_items;
   const int32_t* row_ptr;
   const int32_t* col_idx;
@@ -58,7 +57,8 @@ struct SearchParams {
 cudaError_t launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                         const AttnParams& p, int head_dim, bool two, bool sparse, int num_sms,
                         cudaStream_t st);
-// d = 128 on a CTA pair (attn2_fwd.cu): dense items of 512 rows, sparse (block 128) items of 4 q-blocks.
+// d = 128 on a CTA pair (attn_pair.cu): same items and kv streams as launch_attn (two 128-row q
+// tiles per item), one tile per SM of the pair.
 cudaError_t launch_attn_pair(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                              const AttnParams& p, bool sparse, int num_sms, cudaStream_t st);
 cudaError_t launch_sparse_prep(const SparsePrepParams& p, cudaStream_t st);

@@ -68,12 +68,12 @@ __device__ __forceinline__ uint32_t s_col(int t) { return static_cast<uint32_t>(
 __device__ __forceinline__ uint32_t o_col(int t) { return 256u + static_cast<uint32_t>(t) * 128u; }
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef ADASPA_EXP_POLY_MOD
-#define ADASPA_EXP_POLY_MOD 0
+#define ADASPA_EXP_POLY_MOD 8
 #endif
 #ifndef ADASPA_ABLATE
-#define ADASPA_ABLATE 0  // diagnostic builds only: 4 = no softmax, 5 = no softmax + one shared Q tile
+#define ADASPA_ABLATE 0  // diagnostic builds only: 4 = no softmax (MMA / TMA pipeline alone)
 #endif
-constexpr int kExpPolyMod = ADASPA_EXP_POLY_MOD;  // one pair in kExpPolyMod on the FMA-pipe polynomial (0: none)
+constexpr int kExpPolyMod = ADASPA_EXP_POLY_MOD;  // one group in kExpPolyMod on the FMA-pipe polynomial (0: none; 8 measured best)
 
 enum : int { kNormal = 0, kEnd = 1, kAllEnd = 2 };
 
@@ -99,11 +99,13 @@ template <int D>
 struct Smem {
   static constexpr int kTile = 128 * D * 2;  // one 128-row tile of d bf16 columns
   // ADASPA_ABLATE 5 (diagnostic): one shared Q tile, 5 K/V slots -- pipeline depth experiment
-  static constexpr int kNS = (D == 128) ? (ADASPA_ABLATE == 5 ? 5 : 4) : 10;
+  // d=128: Q (64 KB) + 5 K/V slots (160 KB) + barriers fill the 227 KB; 5 slots let the producer
+  // run ~2.5 entries ahead (with 4, the MMA thread waited ~280 cycles per entry for the next K).
+  static constexpr int kNS = (D == 128) ? 5 : 10;
   static constexpr int kQ = 0;
-  static constexpr int kKV = (ADASPA_ABLATE == 5 ? 1 : 2) * kTile;
+  static constexpr int kKV = 2 * kTile;
   static constexpr int kBar = kKV + kNS * kTile;
-  static constexpr int kBytes = kBar + 6144 + 1024;  // barriers/meta/exchange + alignment slack
+  static constexpr int kBytes = kBar + 2048 + 1024;  // barriers/meta + alignment slack
 };
 
 struct Bars {
@@ -157,6 +159,9 @@ __device__ __forceinline__ void decode_item(const AttnParams& p, bool sparse, bo
     }
   }
 }
+
+static_assert(sizeof(Bars) <= 2048, "barrier block outgrew its reservation");
+static_assert(Smem<128>::kBytes <= 232448 && Smem<64>::kBytes <= 232448, "over 227 KB of shared memory");
 
 template <int D, bool TWO, bool SPARSE>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -227,11 +232,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bars->q_empty, qph ^ 1);
         qph ^= 1;
         bars->qitem = it;
-        const uint32_t qbytes = ADASPA_ABLATE == 5 ? TILE : (it.exists[0] ? TILE : 0) + (it.exists[1] ? TILE : 0);
+        const uint32_t qbytes = (it.exists[0] ? TILE : 0) + (it.exists[1] ? TILE : 0);
         mbar_arrive_expect_tx(&bars->q_full, qbytes);
         for (int t = 0; t < 2; ++t) {
           if (!it.exists[t]) continue;
-          if (ADASPA_ABLATE == 5 && t == 1) continue;
           const int r1 = TWO ? it.start1[t] : it.start0[t] + 64;
           for (int c = 0; c < CH; ++c) {
             uint8_t* dst = sQ + t * TILE + c * CHUNK;
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * CHUNK + (kk & 3) * 32;
-          const uint64_t a = desc_sw128(sq_addr + (ADASPA_ABLATE == 5 ? 0 : t) * TILE + off, 16, 1024);
+          const uint64_t a = desc_sw128(sq_addr + t * TILE + off, 16, 1024);
           const uint64_t b = desc_sw128(skv_addr + kslot * TILE + off, 16, 1024);
           mma_ss(tmem + s_col(t), a, b, kIdescQK, kk > 0 ? 1u : 0u);
         }
@@ -566,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ntile = 0;
         continue;
       }
-      if (ADASPA_ABLATE == 4 || ADASPA_ABLATE == 5) {  // diagnostic: no softmax (MMA/TMA pipeline alone)
+      if (ADASPA_ABLATE == 4) {  // diagnostic: no softmax (MMA/TMA pipeline alone)
         ADASPA_TRACE_EV(1);
         ADASPA_TRACE_EV(2);
         tc_fence_before();
@@ -576,9 +580,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++ntile;
         continue;
       }
-      // valid columns: [0, limA) of kv half 0 and [64, limB) of kv half 1 (absolute, 0..128)
-      const int limA = inf.lim[hq * 2 + 0];
-      const int limB = inf.lim[hq * 2 + 1];
+      // valid columns: [0, limA) of kv half 0 and [64, limB) of kv half 1 (absolute, 0..128); read
+      // (volatile: issued before the TMEM load, not sunk behind it into the MUFU-congested MIO queue)
+      const int limA = *reinterpret_cast<const volatile int*>(&inf.lim[hq * 2 + 0]);
+      const int limB = *reinterpret_cast<const volatile int*>(&inf.lim[hq * 2 + 1]);
       uint32_t s[64];
       tmem_ld_16x256b_x8(s_addr, s);
       tmem_ld_16x256b_x8(s_addr + 64, s + 32);
@@ -608,20 +613,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       float mb[2];
       float alpha[2] = {1.0f, 1.0f};
       bool rescale = false;
+      float lmx[2] = {fmaxf(mxa[0], mxb[0]) * sl2, fmaxf(mxa[1], mxb[1]) * sl2};
+      // m_used only moves when the row max grows past it by more than 2^8, so the quad's row max is
+      // needed only then: one warp vote instead of four shuffles (which queue behind MUFU in MIO).
+      if (__any_sync(0xffffffffu, lmx[0] > m_used[0] + kRescaleThreshold || lmx[1] > m_used[1] + kRescaleThreshold)) {
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        float mx = fmaxf(mxa[j], mxb[j]);
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float m_new = fmaxf(m_used[j], mx * sl2);
-        if (m_new > m_used[j] + kRescaleThreshold) {  // also true when m_used == -inf
-          alpha[j] = (m_used[j] == -INFINITY) ? 0.0f : exp2f(m_used[j] - m_new);
-          l_sum[j] *= alpha[j];
-          m_used[j] = m_new;
-          rescale |= alpha[j] != 0.0f && ntile > 0;
+        for (int j = 0; j < 2; ++j) {
+          float mx = lmx[j];
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+          const float m_new = fmaxf(m_used[j], mx);
+          if (m_new > m_used[j] + kRescaleThreshold) {  // also true when m_used == -inf
+            alpha[j] = (m_used[j] == -INFINITY) ? 0.0f : exp2f(m_used[j] - m_new);
+            l_sum[j] *= alpha[j];
+            m_used[j] = m_new;
+            rescale |= alpha[j] != 0.0f && ntile > 0;
+          }
         }
-        mb[j] = (m_used[j] == -INFINITY) ? 0.0f : m_used[j];
       }
+      mb[0] = (m_used[0] == -INFINITY) ? 0.0f : m_used[0];
+      mb[1] = (m_used[1] == -INFINITY) ? 0.0f : m_used[1];
       ADASPA_TRACE_EV(2);
       if (__any_sync(0xffffffffu, rescale)) {  // rare: the running max grew by more than 2^8
 #pragma unroll 1
@@ -695,7 +706,7 @@ __global__ void __launch_bounds__(256) sparse_stream_kernel(SparsePrepParams p) 
   const int bh = item / p.items_per_bh;
   const int pi = item - bh * p.items_per_bh;
   const int nb = p.grid.nb;
-  const int nq = (p.two || p.quad) ? 4 : 2;
+  const int nq = p.two ? 4 : 2;
   int rbeg[4], rend[4];
   for (int s = 0; s < 4; ++s) {
     const int qb = nq * pi + s;
@@ -739,9 +750,7 @@ __global__ void __launch_bounds__(256) sparse_stream_kernel(SparsePrepParams p) 
       const int j = w * 32 + lane;
       uint32_t memb = 0;
       for (int s = 0; s < 4; ++s) memb |= ((word[s] >> lane) & 1u) << s;
-      if (p.quad) {
-        out[pos] = stream_entry(j, j, memb);  // bit s: q-block 4p + s of the item keeps kv block j
-      } else if (!p.two) {
+      if (!p.two) {
         const uint32_t mask = ((memb & 1u) ? 0x0Fu : 0u) | ((memb & 2u) ? 0xF0u : 0u);
         out[pos] = stream_entry(j, j, mask);
       } else {
