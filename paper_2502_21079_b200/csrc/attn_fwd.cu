@@ -111,7 +111,7 @@ struct Smem {
 struct Bars {
   uint64_t kv_full[12], kv_empty[12];
   uint64_t q_full, q_empty;
-  uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
+  uint64_t s_full[2], p_half[2], p_full[2], o_full[2], o_empty[2];
   SlotMeta meta[12];
   TileInfo info[2][2];
   ItemInfo qitem;
@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars->q_empty, 1);
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bars->s_full[t], 2);
+      mbar_init(&bars->p_half[t], 8);  // P columns [0, 32) (kv rows 0-63) of every row stored
       mbar_init(&bars->p_full[t], 8);
       mbar_init(&bars->o_full[t], 1);
       mbar_init(&bars->o_empty[t], 8);
@@ -326,12 +327,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_ss(tmem + s_col(t), a, b, kIdescQK, kk > 0 ? 1u : 0u);
         }
       };
-      auto issue_pv = [&](int t, int vslot, bool first) {
+      // PV in two halves: kv rows 0-63 (P columns 0-31) as soon as the softmax has stored them,
+      // so they run while it computes the second half; then kv rows 64-127.
+      auto issue_pv_half = [&](int t, int vslot, bool first, int half) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const int kk = 4 * half + k4;
           const uint64_t b = desc_sw128(skv_addr + vslot * TILE + kk * 2048, CHUNK, 1024);
           mma_ts(tmem + o_col(t), tmem + s_col(t) + kk * 8, b, kIdescPV, (first && kk == 0) ? 0u : 1u);
         }
+      };
+      // wait for P_t (both halves) and issue PV_t; O must have been drained by the epilogue first
+      auto wait_issue_pv = [&](int t, int vslot, bool first) {
+        mbar_wait(&bars->p_half[t], pph[t]);
+        tc_fence_after();
+        if (first && o_dirty[t]) {
+          mbar_wait(&bars->o_empty[t], oeph[t]);
+          oeph[t] ^= 1;
+          o_dirty[t] = false;
+          tc_fence_after();
+        }
+        issue_pv_half(t, vslot, first, 0);
+        mbar_wait(&bars->p_full[t], pph[t]);
+        pph[t] ^= 1;
+        tc_fence_after();
+        issue_pv_half(t, vslot, false, 1);
       };
 
       for (;;) {
@@ -365,16 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
               if (!pend[t]) continue;
-              mbar_wait(&bars->p_full[t], pph[t]);
-              pph[t] ^= 1;
-              tc_fence_after();
-              if (first_pv[t] && o_dirty[t]) {
-                mbar_wait(&bars->o_empty[t], oeph[t]);
-                oeph[t] ^= 1;
-                o_dirty[t] = false;
-                tc_fence_after();
-              }
-              issue_pv(t, pvslot, first_pv[t]);
+              wait_issue_pv(t, pvslot, first_pv[t]);
               first_pv[t] = false;
             }
             if (pvslot >= 0) tc_commit(&bars->kv_empty[pvslot]);
@@ -415,17 +426,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             if (pend[t]) {
-              mbar_wait(&bars->p_full[t], pph[t]);
-              pph[t] ^= 1;
+              wait_issue_pv(t, pvslot, first_pv[t]);
               ADASPA_TRACE_MMA(t * 2 + 0);
-              tc_fence_after();
-              if (first_pv[t] && o_dirty[t]) {
-                mbar_wait(&bars->o_empty[t], oeph[t]);
-                oeph[t] ^= 1;
-                o_dirty[t] = false;
-                tc_fence_after();
-              }
-              issue_pv(t, pvslot, first_pv[t]);
               first_pv[t] = false;
               pend[t] = false;
             }
@@ -576,7 +578,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         ADASPA_TRACE_EV(3);
-        if (lane == 0) mbar_arrive(&bars->p_full[t]);
+        if (lane == 0) {
+          mbar_arrive(&bars->p_half[t]);
+          mbar_arrive(&bars->p_full[t]);
+        }
         ++ntile;
         continue;
       }
@@ -676,6 +681,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk[2 * k + 1] = pack_bf16x2(p1.x, p1.y);
         }
         tmem_st_16x128b_x8(s_addr + c * 32, pk);
+        if (c == 0) {  // first half of P stored: the MMA thread may start PV on kv rows 0-63
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars->p_half[t]);
+        }
       }
       const float2 a0 = fadd2(acc[0], acc[2]), a1 = fadd2(acc[1], acc[3]);
       l_sum[0] += a0.x + a0.y;
