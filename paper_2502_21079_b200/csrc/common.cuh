@@ -428,6 +428,33 @@ __device__ __forceinline__ void mma_ts_pair(uint32_t d_tmem, uint32_t a_tmem, ui
       : "memory");
 }
 
+// Degree-5 packed variant (relative error 2.3e-7, ex2.approx's class): for the search's block
+// masses, where the offloaded share must not bias the sums.
+struct Poly5x2 {
+  float2 c0, c1, c2, c3, c4, c5;
+  __device__ __forceinline__ Poly5x2()
+      : c0(make_float2(1.0000001192092896f, 1.0000001192092896f)),
+        c1(make_float2(0.6931469440460205f, 0.6931469440460205f)),
+        c2(make_float2(0.24022120237350464f, 0.24022120237350464f)),
+        c3(make_float2(0.05550713464617729f, 0.05550713464617729f)),
+        c4(make_float2(0.009675541892647743f, 0.009675541892647743f)),
+        c5(make_float2(0.001327645848505199f, 0.001327645848505199f)) {}
+};
+__device__ __forceinline__ float2 exp2_poly5x2(float2 x, const Poly5x2& c) {
+  x.x = fmaxf(x.x, -126.0f);
+  x.y = fmaxf(x.y, -126.0f);
+  const float2 t = fadd2(x, make_float2(12582912.0f, 12582912.0f));
+  const float2 j = fadd2(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = ffma2(j, make_float2(-1.0f, -1.0f), x);
+  float2 p = ffma2(c.c5, f, c.c4);
+  p = ffma2(p, f, c.c3);
+  p = ffma2(p, f, c.c2);
+  p = ffma2(p, f, c.c1);
+  p = ffma2(p, f, c.c0);
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 // Degree-3 variant (relative error 7.5e-5): for P of the attention passes, which is rounded to
 // bf16 (2^-9) before the PV product anyway.
 struct Poly3x2 {

@@ -21,10 +21,11 @@ namespace {
 constexpr int kThreads = 640;
 
 constexpr int kChunk = 256;  // kv tiles per flush of the per-warp partial masses
-#ifndef ADASPA_SEARCH_POLY_MOD
-#define ADASPA_SEARCH_POLY_MOD 8
+#ifndef ADASPA_SEARCH_POLY_MASK
+#define ADASPA_SEARCH_POLY_MASK 0x80
 #endif
-constexpr int kSearchPolyMod = ADASPA_SEARCH_POLY_MOD;  // one pair in this many on the FMA-pipe polynomial
+// bit (i % 8): pair i of a 64-column half goes to the FMA-pipe polynomial instead of MUFU.EX2
+constexpr uint32_t kSearchPolyMask = ADASPA_SEARCH_POLY_MASK;
 
 template <int D>
 struct SSmem {
@@ -110,14 +111,14 @@ __device__ __forceinline__ void kv_tile(const SearchParams& p, bool two, int j, 
 // tree.  (Measured on HYV-110K / CogX-45K: 1 in 8 is best; 1 in 4 or 3 loses to the FMA pipe.)
 template <bool FULL>
 __device__ __forceinline__ float half_mass(const uint32_t* s, float2 sl2, float2 nl, int lim) {
+  const Poly5x2 poly;
   float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sl2, nl);
     float2 e;
-    if (kSearchPolyMod > 0 && (i % (kSearchPolyMod > 0 ? kSearchPolyMod : 1)) == kSearchPolyMod - 1) {
-      e.x = exp2_poly<5>(x.x);
-      e.y = exp2_poly<5>(x.y);
+    if ((kSearchPolyMask >> (i & 7)) & 1u) {
+      e = exp2_poly5x2(x, poly);
     } else {
       e.x = ex2_approx(x.x);
       e.y = ex2_approx(x.y);
