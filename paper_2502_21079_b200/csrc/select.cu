@@ -82,25 +82,34 @@ __global__ void __launch_bounds__(256, KPL <= 32 ? 3 : 1) select_rows_kernel(Sel
   const int t0 = p.text_first ? 0 : p.grid.nb_first;
   const int t1 = p.text_first ? p.grid.nb_first : nb;
 
-  // element i of this lane is kv-block j = 32 i + lane; cmask / fmask: candidate / forced bits
+  // element i of this lane is kv-block j = 32 i + lane (KPL is up to 128 elements per lane, so the
+  // candidate / forced status is recomputed from j rather than kept in a 32-bit mask)
+  auto is_forced = [&](int i) -> bool {
+    const int j = i * 32 + lane;
+    return j < nb && p.text_sink && j >= t0 && j < t1;
+  };
+  auto is_cand = [&](int i) -> bool {
+    const int j = i * 32 + lane;
+    return j < nb && !(p.text_sink && j >= t0 && j < t1);
+  };
   float m[KPL];
-  uint32_t cmask = 0u, fmask = 0u;
+  int ncand_l = 0, nforced_l = 0;
   double tsum = 0.0, fsum = 0.0;
 #pragma unroll
   for (int i = 0; i < KPL; ++i) {
     const int j = i * 32 + lane;
     const bool valid = j < nb;
     const float x = valid ? __ldg(mrow + j) : 0.0f;
-    const bool forced = valid && p.text_sink && j >= t0 && j < t1;
+    const bool forced = is_forced(i);
     tsum += f2d_volatile(x);
     if (forced) fsum += f2d_volatile(x);
-    cmask |= (valid && !forced) ? (1u << i) : 0u;
-    fmask |= forced ? (1u << i) : 0u;
-    m[i] = (valid && !forced) ? x : 0.0f;  // candidate masses only (forced mass is F)
+    ncand_l += is_cand(i) ? 1 : 0;
+    nforced_l += forced ? 1 : 0;
+    m[i] = is_cand(i) ? x : 0.0f;  // candidate masses only (forced mass is F)
   }
   const double T = warp_sum_f64(tsum);
   const double F = warp_sum_f64(fsum);
-  const int ncand = warp_sum_i32(__popc(cmask));
+  const int ncand = warp_sum_i32(ncand_l);
 
   // decision: 0 = keep all, 1 = forced only (+top-1 if none forced), 2 = cut at v*
   int decision;
@@ -141,7 +150,7 @@ __global__ void __launch_bounds__(256, KPL <= 32 ? 3 : 1) select_rows_kernel(Sel
 #pragma unroll
       for (int i = 0; i < KPL; ++i) {
         const uint32_t b = __float_as_uint(m[i]);
-        const bool c = (cmask >> i) & 1u;
+        const bool c = is_cand(i);
         bmin = c && b < bmin ? b : bmin;
         bmax = c && b > bmax ? b : bmax;
       }
@@ -223,7 +232,7 @@ __global__ void __launch_bounds__(256, KPL <= 32 ? 3 : 1) select_rows_kernel(Sel
 #pragma unroll
       for (int i = 0; i < KPL; ++i) {
         const uint32_t b = __float_as_uint(m[i]);
-        const bool c = (cmask >> i) & 1u;
+        const bool c = is_cand(i);
         if (c && b > vstar) {
           sgt += f2d_volatile(m[i]);
           ++cgt;
@@ -251,14 +260,14 @@ __global__ void __launch_bounds__(256, KPL <= 32 ? 3 : 1) select_rows_kernel(Sel
 
   // top-1 candidate for decision 1 with an empty forced set (reading R25)
   int top1 = -1;
-  if (decision == 1 && warp_sum_i32(__popc(fmask)) == 0) {
+  if (decision == 1 && warp_sum_i32(nforced_l) == 0) {
     uint32_t best = 0u;
     int bj = 0x7fffffff;
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {
       const int j = i * 32 + lane;
       const uint32_t b = __float_as_uint(m[i]);
-      if (((cmask >> i) & 1u) && (b > best || (b == best && j < bj))) {
+      if (is_cand(i) && (b > best || (b == best && j < bj))) {
         best = b;
         bj = j;
       }
@@ -283,8 +292,8 @@ __global__ void __launch_bounds__(256, KPL <= 32 ? 3 : 1) select_rows_kernel(Sel
 #pragma unroll
   for (int i = 0; i < KPL; ++i) {
     const int j = i * 32 + lane;
-    const bool cand = (cmask >> i) & 1u;
-    const bool forced = (fmask >> i) & 1u;
+    const bool cand = is_cand(i);
+    const bool forced = is_forced(i);
     bool keep;
     if (decision == 0) {
       keep = j < nb;

@@ -1,4 +1,4 @@
-"""Parity of the CTA-pair kernel (run with ADASPA_PAIR=1; used by tests/test_gpu_pair.py):
+"""Test infrastructure (run by tests/test_gpu_pair.py with ADASPA_PAIR=1): parity of the CTA-pair kernel:
 K1 dense and K4 block-sparse at d=128, block 128, several 256-row pair items per head, both text
 orders, batch 2, against the fp64 oracle (tolerances of tests/gpu_helpers.py)."""
 import math

@@ -1,6 +1,6 @@
 """The CTA-pair kernel (attn_pair.cu, cta_group::2; opt-in with ADASPA_PAIR=1) against
 the fp64 oracle.  The library reads ADASPA_PAIR once per process, so each case runs in a fresh
-interpreter (tools/pair_check.py) with the variable set."""
+interpreter (tests/pair_check.py) with the variable set."""
 
 import os
 import subprocess
@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.parametrize("case", ["dense", "sparse"])
 def test_pair_kernel_matches_oracle(case):
     env = dict(os.environ, ADASPA_PAIR="1")
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "pair_check.py"), case],
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "pair_check.py"), case],
                        env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "pair ok" in r.stdout

@@ -135,6 +135,40 @@ def test_select_blocks_exact(ada, tf, mode):
     assert (np.diff(cnt[order]) <= 0).all()
 
 
+@pytest.mark.parametrize("nv,nt", [(70000, 226), (150000, 256), (261000, 256)])
+@pytest.mark.parametrize("mode", ["recall", "sparsity"])
+def test_select_blocks_exact_large_nb(ada, nv, nt, mode):
+    """K3 at nb > 1024 (more than 32 kv-blocks per warp lane: nb = 1098 / 2348 / 4082 at block 64,
+    the range the length sweep reaches); sampled rows (every text row, the first and last video
+    rows, seeded random rows) bit-exact against the oracle's per-row selection."""
+    H, B = 2, 64
+    blocks = oracle.block_map(nv, nt, B, False)
+    nb = len(blocks)
+    Mt = workloads.random_masses(H * nb, nb, seed=11).view(1, H, nb, nb)
+    q = torch.empty(1, H, nv + nt, 64, dtype=torch.bfloat16, device="cuda")
+    desc = ada.make_desc(q, B, nt, False)
+    targets = [0.9, 0.5] if mode == "recall" else [0.9, 0.8]
+    kmode = ada.SELECT_RECALL if mode == "recall" else ada.SELECT_SPARSITY
+    out = ada.select_blocks(Mt.cuda(), heads_desc=desc, mode=kmode, target=targets, flags=1)
+    torch.cuda.synchronize()
+    rp = out.row_ptr.cpu().numpy()
+    ci = out.col_idx.cpu().numpy()
+    rng = np.random.default_rng(3)
+    text = [i for i, b in enumerate(blocks) if b.modality == "text"]
+    sample = sorted({0, nb - len(text) - 1, *text, *rng.choice(nb, 40, replace=False).tolist()})
+    for h in range(H):
+        for p in sample:
+            forced, cands = oracle.row_forced_and_candidates(blocks, p, True)
+            m = Mt[0, h, p].double().numpy()
+            if mode == "recall":
+                exp = oracle.select_row_recall(m, forced, cands, targets[h])
+            else:
+                exp = oracle.select_row_sparsity(m, forced, cands, oracle.k_from_sparsity(targets[h], nb - len(text)))
+            row = h * nb + p
+            got = ci[rp[row]:rp[row + 1]].tolist()
+            assert got == exp, f"nb={nb} {mode} h{h} row {p}: {len(got)} kept vs {len(exp)} (first {got[:6]} / {exp[:6]})"
+
+
 def _random_csr(H, nb, density, seed):
     g = np.random.default_rng(seed)
     keep = g.random((H, nb, nb)) < density

@@ -41,13 +41,8 @@ ws = torch.empty(ada.sparse_workspace_bytes(desc), dtype=torch.uint8, device="cu
 o2, _ = ada.block_sparse_attn(q, k, v, out.row_ptr, out.col_idx, workspace=ws, **kw)
 t4 = timeit(lambda: ada.block_sparse_attn(q, k, v, out.row_ptr, out.col_idx, o=o2, workspace=ws, **kw), 5)
 # kept FLOPs: 4 d sum |qb||kb| over kept pairs
-import numpy as np
-import oracle
-blocks = oracle.block_map(lay.n_video, lay.n_text, lay.block, lay.text_first)
-L = torch.tensor([b.length for b in blocks], dtype=torch.float64, device="cuda")
-rp = out.row_ptr.long(); ci = out.col_idx[:nnz].long()
-rows = torch.repeat_interleave(torch.arange(H*nb, device="cuda"), rp[1:]-rp[:-1])
-kept = (L[rows % nb] * L[ci]).sum().item()
+from bench import kept_flops
+kept = kept_flops(lay, out, 1)[0] / 4.0
 kfl = 4.0 * d * kept
 print(f"K4 sparse: {t4:.2f} ms  effective {kfl/t4/1e9:.1f} TFLOP/s (kept FLOPs {kfl/1e12:.2f} TF)", flush=True)
 print(f"search overhead (K2+K3)/K1 = {(t2+t3)/t1:.3f}")
