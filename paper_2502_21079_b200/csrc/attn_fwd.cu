@@ -709,10 +709,37 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ------------------------------------------------------------------ sparse schedule prep
 // One warp per work item: union of the item's CSR rows (2 q-blocks at B=128, 4 at B=64) as a
-// bitmap pass over kv-block words, emitted in ascending order with membership masks.
+// bitmap pass over kv-block words, emitted with membership masks.  B=128: one kv block per entry,
+// ascending.  B=64: an entry pairs two kv blocks into one 128-row tile and a q tile computes the
+// whole tile if either of its q-blocks keeps either block, so blocks are grouped by membership
+// pattern (which of the 4 q-blocks keep them; ascending within a group) before pairing -- in id
+// order 25% of the executed tile work was on dropped pairs (tools/sparse_efficiency.py).
+__device__ __forceinline__ void stream_word(const SparsePrepParams& p, int w, int lane, int* cur, const int* rend,
+                                            uint32_t* word) {
+  for (int s = 0; s < 4; ++s) {
+    uint32_t acc = 0;
+    // lane-parallel: each lane checks one candidate element of list s in this word
+    while (true) {
+      const int idx = cur[s] + lane;
+      int v = (idx < rend[s]) ? p.col_idx[idx] : 0x7fffffff;
+      const bool in = v < (w + 1) * 32;
+      if (in) acc |= 1u << (v - w * 32);
+      const uint32_t bal = __ballot_sync(0xffffffffu, in);
+      const int n_in = __popc(bal);
+      cur[s] += n_in;
+      if (n_in < 32) break;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc |= __shfl_xor_sync(0xffffffffu, acc, o);
+    word[s] = acc;
+  }
+}
+
 __global__ void __launch_bounds__(256) sparse_stream_kernel(SparsePrepParams p) {
+  __shared__ int grp[8][2][16];  // per warp: pattern counts, then running positions
   const int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  const int wl = threadIdx.x >> 5;
   if (item >= p.num_items) return;
   const int bh = item / p.items_per_bh;
   const int pi = item - bh * p.items_per_bh;
@@ -731,47 +758,63 @@ __global__ void __launch_bounds__(256) sparse_stream_kernel(SparsePrepParams p) 
   }
   uint32_t* out = p.stream + static_cast<int64_t>(item) * p.stream_stride;
   const int nwords = (nb + 31) / 32;
-  // cursors into each sorted list, advanced word by word (every lane walks all lists; lists are short)
-  int cur[4] = {rbeg[0], rbeg[1], rbeg[2], rbeg[3]};
+  int cur[4];
+  if (p.two) {
+    // pass 1: how many union blocks have each membership pattern (1..15)
+    if (lane < 16) grp[wl][0][lane] = 0;
+    __syncwarp();
+    for (int s = 0; s < 4; ++s) cur[s] = rbeg[s];
+    for (int w = 0; w < nwords; ++w) {
+      uint32_t word[4];
+      stream_word(p, w, lane, cur, rend, word);
+      uint32_t memb = 0;
+      for (int s = 0; s < 4; ++s) memb |= ((word[s] >> lane) & 1u) << s;
+      const uint32_t same = __match_any_sync(0xffffffffu, memb);
+      if (memb && lane == __ffs(same) - 1) grp[wl][0][memb] += __popc(same);
+      __syncwarp();
+    }
+    // exclusive prefix over patterns -> running positions
+    if (lane == 0) {
+      int acc = 0;
+      for (int m = 0; m < 16; ++m) {
+        grp[wl][1][m] = acc;
+        acc += grp[wl][0][m];
+      }
+    }
+    __syncwarp();
+  }
+  // emit (B=128: ascending union; B=64: pattern groups, ascending within a group)
+  for (int s = 0; s < 4; ++s) cur[s] = rbeg[s];
   int u_count = 0;  // union elements emitted so far
   for (int w = 0; w < nwords; ++w) {
     uint32_t word[4];
-    for (int s = 0; s < 4; ++s) {
-      uint32_t acc = 0;
-      // lane-parallel: each lane checks one candidate element of list s in this word
-      while (true) {
-        const int idx = cur[s] + lane;
-        int v = (idx < rend[s]) ? p.col_idx[idx] : 0x7fffffff;
-        const bool in = v < (w + 1) * 32;
-        if (in) acc |= 1u << (v - w * 32);
-        const uint32_t bal = __ballot_sync(0xffffffffu, in);
-        const int n_in = __popc(bal);
-        cur[s] += n_in;
-        if (n_in < 32) break;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc |= __shfl_xor_sync(0xffffffffu, acc, o);
-      word[s] = acc;
-    }
+    stream_word(p, w, lane, cur, rend, word);
     const uint32_t uni = word[0] | word[1] | word[2] | word[3];
     const bool mine = (uni >> lane) & 1u;
     const uint32_t bal = __ballot_sync(0xffffffffu, mine);
-    if (mine) {
-      const int pos = u_count + __popc(bal & ((1u << lane) - 1u));
-      const int j = w * 32 + lane;
-      uint32_t memb = 0;
-      for (int s = 0; s < 4; ++s) memb |= ((word[s] >> lane) & 1u) << s;
-      if (!p.two) {
+    uint32_t memb = 0;
+    for (int s = 0; s < 4; ++s) memb |= ((word[s] >> lane) & 1u) << s;
+    const int j = w * 32 + lane;
+    if (!p.two) {
+      if (mine) {
+        const int pos = u_count + __popc(bal & ((1u << lane) - 1u));
         const uint32_t mask = ((memb & 1u) ? 0x0Fu : 0u) | ((memb & 2u) ? 0xF0u : 0u);
         out[pos] = stream_entry(j, j, mask);
-      } else {
+      }
+    } else {
+      const uint32_t same = __match_any_sync(0xffffffffu, memb);
+      const int pos = grp[wl][1][memb] + __popc(same & ((1u << lane) - 1u));
+      __syncwarp();
+      if (mine) {
         const int hf = pos & 1;
         uint32_t mask = 0;
         for (int s = 0; s < 4; ++s)
           if ((memb >> s) & 1u) mask |= 1u << (2 * s + hf);  // bit 4t + 2hq + hf with s = 2t + hq
         const uint32_t part = (static_cast<uint32_t>(j) << (12 * hf)) | (mask << 24);
         atomicOr(out + (pos >> 1), part);
+        if (lane == __ffs(same) - 1) grp[wl][1][memb] += __popc(same);
       }
+      __syncwarp();
     }
     u_count += __popc(bal);
   }
