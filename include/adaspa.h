@@ -155,6 +155,8 @@ size_t adaspa_select_workspace_bytes(const adaspa_attn_desc* desc);
  *              counts unspecified).
  * head_recall: fp32 [B,H] output or NULL: achieved Recall per head.
  * head_nnz   : int64 [B,H] output or NULL: kept blocks per head.
+ * Limits: nb <= 6144 (one warp holds a row) and B*H*nb*nb < 2^31, else
+ * ADASPA_ERR_UNSUPPORTED.
  */
 adaspa_status adaspa_select_blocks(const adaspa_attn_desc* desc, const float* block_mass,
                                    adaspa_select_mode mode, const double* target, uint32_t flags,
@@ -171,7 +173,8 @@ size_t adaspa_sparse_workspace_bytes(const adaspa_attn_desc* desc);
  * (PAPER.md:415-427 with c = +inf, visiting only kept blocks):
  * for query i of q-block p, J = tokens of the kv-blocks in CSR row p,
  *   lse'_i = log sum_{t in J} exp(S_it),  O_i = sum_{t in J} exp(S_it - lse'_i) V_t.
- * row_ptr / col_idx: the CSR of adaspa_select_blocks (ids ascending, < nb).
+ * row_ptr / col_idx: the CSR of adaspa_select_blocks (ids ascending, < nb);
+ *            nb <= 65535 (16-bit block ids in the kv stream), else ADASPA_ERR_UNSUPPORTED.
  * o: bf16 output.  lse: fp32 [B,H,N] output ("sparse LSE") or NULL.
  * workspace: device scratch of >= adaspa_sparse_workspace_bytes(desc) bytes
  * (the per-launch work schedule is built there).

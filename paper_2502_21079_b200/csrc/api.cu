@@ -170,7 +170,7 @@ SparseWs sparse_ws_layout(const adaspa_attn_desc* d) {
   w.queue = off; off = align256(off + 4);
   w.len = off; off = align256(off + (size_t)w.num_items * 4);
   w.order = off; off = align256(off + (size_t)w.num_items * 4);
-  w.stream = off; off = align256(off + (size_t)w.num_items * w.stride * 4);
+  w.stream = off; off = align256(off + (size_t)w.num_items * w.stride * 8);
   w.bytes = off;
   return w;
 }
@@ -277,7 +277,7 @@ adaspa_status adaspa_select_blocks(const adaspa_attn_desc* desc, const float* bl
   if (flags & ~3u) return fail(ADASPA_ERR_INVALID_ARG, "unknown flag bits 0x%x", flags);
   if (desc->heads > kMaxHeads) return fail(ADASPA_ERR_UNSUPPORTED, "heads > %d", kMaxHeads);
   const BlockGrid g = make_grid(desc);
-  if (g.nb > 4096) return fail(ADASPA_ERR_UNSUPPORTED, "nb = %d > 4096 blocks", g.nb);
+  if (g.nb > kMaxSelectBlocks) return fail(ADASPA_ERR_UNSUPPORTED, "nb = %d > %d blocks", g.nb, kMaxSelectBlocks);
   const int64_t rows = (int64_t)desc->batch * desc->heads * g.nb;
   const int64_t need_cap = rows * g.nb;
   if (need_cap > INT32_MAX) return fail(ADASPA_ERR_UNSUPPORTED, "B*H*nb*nb exceeds int32 CSR indexing");
@@ -382,7 +382,7 @@ adaspa_status adaspa_block_sparse_attn(const adaspa_attn_desc* desc, const void*
     return s;
   if (!row_ptr || !col_idx) return fail(ADASPA_ERR_INVALID_ARG, "row_ptr / col_idx must not be NULL");
   const BlockGrid g = make_grid(desc);
-  if (g.nb > 4095) return fail(ADASPA_ERR_UNSUPPORTED, "nb = %d > 4095 blocks", g.nb);
+  if (g.nb > kMaxSparseBlocks) return fail(ADASPA_ERR_UNSUPPORTED, "nb = %d > %d blocks", g.nb, kMaxSparseBlocks);
   const SparseWs w = sparse_ws_layout(desc);
   if (!workspace || workspace_bytes < w.bytes)
     return fail(ADASPA_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", workspace_bytes, w.bytes);
@@ -406,7 +406,7 @@ adaspa_status adaspa_block_sparse_attn(const adaspa_attn_desc* desc, const void*
   pp.num_items = w.num_items;
   pp.row_ptr = row_ptr;
   pp.col_idx = col_idx;
-  pp.stream = reinterpret_cast<uint32_t*>(ws + w.stream);
+  pp.stream = reinterpret_cast<uint64_t*>(ws + w.stream);
   pp.stream_len = reinterpret_cast<int*>(ws + w.len);
   pp.item_order = reinterpret_cast<int*>(ws + w.order);
   pp.stream_stride = w.stride;

@@ -7,11 +7,15 @@
 namespace adaspa {
 
 // A stream entry of the block-sparse kernel: one 128-row kv tile made of one B=128 block
-// (id0) or two B=64 blocks (id0, id1), plus an 8-bit membership mask.  Mask bit
-// (4*t + 2*hq + hf) says that the 64-row half hq of q-tile t needs kv half hf.
-__host__ __device__ __forceinline__ uint32_t stream_entry(int id0, int id1, uint32_t mask) {
-  return static_cast<uint32_t>(id0) | (static_cast<uint32_t>(id1) << 12) | (mask << 24);
+// (id0) or two B=64 blocks (id0, id1; 16 bits each), plus an 8-bit membership mask in bits 32-39.
+// Mask bit (4*t + 2*hq + hf) says that the 64-row half hq of q-tile t needs kv half hf.
+__host__ __device__ __forceinline__ uint64_t stream_entry(int id0, int id1, uint32_t mask) {
+  return static_cast<uint64_t>(id0) | (static_cast<uint64_t>(id1) << 16) | (static_cast<uint64_t>(mask) << 32);
 }
+__host__ __device__ __forceinline__ int entry_id0(uint64_t e) { return static_cast<int>(e & 0xFFFFu); }
+__host__ __device__ __forceinline__ int entry_id1(uint64_t e) { return static_cast<int>((e >> 16) & 0xFFFFu); }
+__host__ __device__ __forceinline__ uint32_t entry_mask(uint64_t e) { return static_cast<uint32_t>(e >> 32); }
+constexpr int kMaxSparseBlocks = 65535;
 
 struct AttnParams {
   int B, H, N;
@@ -24,7 +28,7 @@ struct AttnParams {
   int items_per_bh;
   // block-sparse only
   const int* item_order;     // [num_items]: processing order (head-major, longest first in a head)
-  const uint32_t* stream;    // [num_items, stream_stride]
+  const uint64_t* stream;    // [num_items, stream_stride]
   const int* stream_len;     // [num_items]
   int stream_stride;
   int* queue;                // atomic work counter
@@ -37,7 +41,7 @@ struct SparsePrepParams {
   int items_per_bh, num_items;
   const int32_t* row_ptr;
   const int32_t* col_idx;
-  uint32_t* stream;
+  uint64_t* stream;
   int* stream_len;
   int* item_order;
   int stream_stride;

@@ -245,15 +245,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         const int n_ent = SPARSE ? __ldg(p.stream_len + id) : (p.N + 127) / 128;
-        const uint32_t* ent_ptr = SPARSE ? p.stream + static_cast<int64_t>(id) * p.stream_stride : nullptr;
+        const uint64_t* ent_ptr = SPARSE ? p.stream + static_cast<int64_t>(id) * p.stream_stride : nullptr;
         const uint32_t dense_mask = (it.exists[0] ? 0x0Fu : 0u) | (it.exists[1] ? 0xF0u : 0u);
         for (int e = 0; e < n_ent; ++e) {
           int s0, l0, s1, l1;
           uint32_t mask;
           if (SPARSE) {
-            const uint32_t ent = __ldg(ent_ptr + e);
-            const int id0 = ent & 0xFFF, id1 = (ent >> 12) & 0xFFF;
-            mask = ent >> 24;
+            const uint64_t ent = __ldg(reinterpret_cast<const unsigned long long*>(ent_ptr) + e);
+            const int id0 = entry_id0(ent), id1 = entry_id1(ent);
+            mask = entry_mask(ent);
             s0 = p.grid.start(id0);
             l0 = p.grid.len(id0);
             if (TWO) {
@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(256) sparse_stream_kernel(SparsePrepParams p) 
       rbeg[s] = rend[s] = 0;
     }
   }
-  uint32_t* out = p.stream + static_cast<int64_t>(item) * p.stream_stride;
+  uint64_t* out = p.stream + static_cast<int64_t>(item) * p.stream_stride;
   const int nwords = (nb + 31) / 32;
   int cur[4];
   if (p.two) {
@@ -810,8 +810,8 @@ __global__ void __launch_bounds__(256) sparse_stream_kernel(SparsePrepParams p) 
         uint32_t mask = 0;
         for (int s = 0; s < 4; ++s)
           if ((memb >> s) & 1u) mask |= 1u << (2 * s + hf);  // bit 4t + 2hq + hf with s = 2t + hq
-        const uint32_t part = (static_cast<uint32_t>(j) << (12 * hf)) | (mask << 24);
-        atomicOr(out + (pos >> 1), part);
+        const uint64_t part = (static_cast<uint64_t>(j) << (16 * hf)) | (static_cast<uint64_t>(mask) << 32);
+        atomicOr(reinterpret_cast<unsigned long long*>(out + (pos >> 1)), static_cast<unsigned long long>(part));
         if (lane == __ffs(same) - 1) grp[wl][1][memb] += __popc(same);
       }
       __syncwarp();
@@ -824,8 +824,8 @@ __global__ void __launch_bounds__(256) sparse_stream_kernel(SparsePrepParams p) 
     if (p.two) {
       n = (u_count + 1) / 2;
       if (u_count & 1) {  // odd union: duplicate id0 into the empty half (mask bits stay 0)
-        const uint32_t e = out[n - 1];
-        out[n - 1] = e | ((e & 0xFFFu) << 12);
+        const uint64_t e = out[n - 1];
+        out[n - 1] = e | (static_cast<uint64_t>(entry_id0(e)) << 16);
       }
     }
     p.stream_len[item] = n;
@@ -859,7 +859,7 @@ extern "C" int adaspa_debug_trace(unsigned long long* host, int n) {
 #endif
 
 cudaError_t launch_sparse_prep(const SparsePrepParams& p, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(p.stream, 0, sizeof(uint32_t) * static_cast<size_t>(p.num_items) * p.stream_stride, st);
+  cudaError_t e = cudaMemsetAsync(p.stream, 0, sizeof(uint64_t) * static_cast<size_t>(p.num_items) * p.stream_stride, st);
   if (e != cudaSuccess) return e;
   const int blocks = (p.num_items * 32 + 255) / 256;
   sparse_stream_kernel<<<blocks, 256, 0, st>>>(p);

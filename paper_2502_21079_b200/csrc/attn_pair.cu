@@ -126,14 +126,14 @@ __device__ __forceinline__ void decode_item3(const AttnParams& p, int id, Item3&
 
 // kv rows of step e: start and valid length; membership mask (bits 0-3: tile 0, 4-7: tile 1)
 template <bool SPARSE>
-__device__ __forceinline__ void step_kv(const AttnParams& p, const uint32_t* ent_ptr, int e, int& s0, int& l0,
+__device__ __forceinline__ void step_kv(const AttnParams& p, const uint64_t* ent_ptr, int e, int& s0, int& l0,
                                         uint32_t& mask) {
   if (SPARSE) {
-    const uint32_t ent = __ldg(ent_ptr + e);
-    const int j = ent & 0xFFF;
+    const uint64_t ent = __ldg(reinterpret_cast<const unsigned long long*>(ent_ptr) + e);
+    const int j = entry_id0(ent);
     s0 = p.grid.start(j);
     l0 = p.grid.len(j);
-    mask = ent >> 24;
+    mask = entry_mask(ent);
   } else {
     s0 = 128 * e;
     l0 = p.N - s0 < 128 ? p.N - s0 : 128;
@@ -242,7 +242,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int qs = rr ? it.start[1] : it.start[0];
 #pragma unroll
       for (int c = 0; c < 2; ++c) tma_load_4d_pair(&tq, q_full_l, sQ + c * kChunkQ, c * 64, qs, it.h, it.b, pol_q);
-      const uint32_t* ent_ptr = SPARSE ? p.stream + static_cast<int64_t>(id) * p.stream_stride : nullptr;
+      const uint64_t* ent_ptr = SPARSE ? p.stream + static_cast<int64_t>(id) * p.stream_stride : nullptr;
       const int n = it.n_ent;
       auto load_k = [&](int e) {
         int s0, l0;

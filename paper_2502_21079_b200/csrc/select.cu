@@ -484,7 +484,8 @@ static cudaError_t launch_rows(const SelectRowsParams& p, cudaStream_t st) {
   else if (kpl <= 28) select_rows_kernel<28><<<blocks, threads, 0, st>>>(p);
   else if (kpl <= 32) select_rows_kernel<32><<<blocks, threads, 0, st>>>(p);
   else if (kpl <= 64) select_rows_kernel<64><<<blocks, threads, 0, st>>>(p);
-  else select_rows_kernel<128><<<blocks, threads, 0, st>>>(p);
+  else if (kpl <= 128) select_rows_kernel<128><<<blocks, threads, 0, st>>>(p);
+  else select_rows_kernel<kMaxSelectBlocks / 32><<<blocks, threads, 0, st>>>(p);  // spills; K3 is <0.1% of a step
   return cudaGetLastError();
 }
 

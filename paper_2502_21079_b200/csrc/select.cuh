@@ -74,5 +74,6 @@ struct SelectLaunch {
 cudaError_t launch_select(const SelectLaunch& L, cudaStream_t st);
 
 __host__ __device__ int k_from_sparsity(double s, int n);
+constexpr int kMaxSelectBlocks = 6144;  // one warp holds a row: 192 masses per lane at most
 
 }  // namespace adaspa

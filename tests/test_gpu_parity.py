@@ -202,6 +202,35 @@ def test_block_sparse_attn(ada, name, over, density):
         compare_out(o[0, h], ro, lse[0, h], rl, what=f"{name} d={density} h{h}")
 
 
+def test_block_sparse_attn_large_nb(ada):
+    """K4 with block ids above 4095 (16-bit ids in the kv stream): nb = 4202 at block 64, a seeded
+    CSR of ~1.5% density in which every sampled row also keeps blocks >= 4096; sampled q-blocks
+    against the oracle's masked attention (one q-block at a time)."""
+    lay = workloads.layout_for("tiny", f=16, h=16, w=1050, n_text=77, head_dim=64, block=64, heads=1)
+    q, k, v = _qkv(lay)
+    blocks = oracle.block_map(lay.n_video, lay.n_text, lay.block, lay.text_first)
+    nb = len(blocks)
+    assert nb > 4096
+    g = np.random.default_rng(17)
+    rows = []
+    for p in range(nb):
+        ids = set(g.choice(nb, 60, replace=False).tolist())
+        ids.add(int(g.integers(4096, nb)))
+        rows.append(sorted(ids))
+    rp = torch.tensor(np.cumsum([0] + [len(r) for r in rows]), dtype=torch.int32, device="cuda")
+    ci = torch.tensor([j for r in rows for j in r], dtype=torch.int32, device="cuda")
+    o, lse = ada.block_sparse_attn(q, k, v, rp, ci, block_size=lay.block, n_text=lay.n_text,
+                                   text_first=lay.text_first, want_lse=True)
+    torch.cuda.synchronize()
+    scale = 1 / math.sqrt(lay.head_dim)
+    qh, kh, vh = np64(q[0, 0]), np64(k[0, 0]), np64(v[0, 0])
+    for p in sorted({0, 4095, 4096, nb - 1, *g.choice(nb, 8, replace=False).tolist()}):
+        b = blocks[p]
+        r = slice(b.start, b.start + b.length)
+        ro, rl = oracle.masked_attention(qh, kh, vh, blocks, {p: rows[p]}, scale, q_block_ids=[p])
+        compare_out(o[0, 0, r], ro, lse[0, 0, r], rl, what=f"large-nb K4 qb{p}")
+
+
 def test_end_to_end_tiny(ada):
     """K1 -> K2 (fresh LSE) -> K3 (recall 0.9) -> K4 against the oracle pipeline, both text orders."""
     for name in ("tiny", "tiny_tf"):
