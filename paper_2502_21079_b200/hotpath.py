@@ -74,7 +74,7 @@ class HotPath:
     def kernels_per_run(self):
         return 9 + (2 if self.flags & L.FLAG_HEAD_TIERS else 0)
 
-    def run_sparse_host(self, q_host, k_host, v_host, o_host, groups=4):
+    def run_sparse_host(self, q_host, k_host, v_host, o_host, groups=12):
         """A sparse denoising step end to end from host memory (the steps between
         key steps only run the block-sparse forward on the cached index lists): per head group, the
         H2D copy of Q,K,V on a copy stream overlaps K4 of the previous group on the current stream,
