@@ -104,6 +104,15 @@ def _stream(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
+def _scratch(nbytes, device, stream):
+    """Scratch owned by one call: if the call runs on a stream other than the current one, tell the
+    caching allocator, so that the block is not handed out again before that stream is done."""
+    t = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    if stream is not None and stream != torch.cuda.current_stream(device):
+        t.record_stream(stream)
+    return t
+
+
 def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
@@ -186,7 +195,7 @@ def select_blocks(block_mass, *, heads_desc, mode, target, flags=FLAG_TEXT_SINK,
                   torch.empty(B, H, dtype=torch.float32, device=dev),
                   torch.empty(B, H, dtype=torch.int64, device=dev))
     wsb = int(_lib.adaspa_select_workspace_bytes(ctypes.byref(desc)))
-    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    ws = _scratch(max(wsb, 1), dev, stream)
     _check(_lib.adaspa_select_blocks(ctypes.byref(desc), _ptr(block_mass), int(mode), tarr, int(flags),
                                      float(tier_tau), _ptr(out.row_ptr), _ptr(out.col_idx), out.col_idx.numel(),
                                      _ptr(out.row_order), _ptr(out.head_recall), _ptr(out.head_nnz), _ptr(ws),
@@ -212,9 +221,12 @@ def block_sparse_attn(q, k, v, row_ptr, col_idx, *, block_size, n_text, text_fir
     for t, nm in ((row_ptr, "row_ptr"), (col_idx, "col_idx")):
         if t.dtype != torch.int32 or not t.is_cuda or not t.is_contiguous():
             raise ValueError(f"{nm} must be a contiguous int32 CUDA tensor")
+    rows = desc.batch * desc.heads * num_blocks(desc)
+    if row_ptr.numel() < rows + 1:
+        raise ValueError(f"row_ptr has {row_ptr.numel()} entries, the CSR needs B*H*nb+1 = {rows + 1}")
     wsb = sparse_workspace_bytes(desc)
     if workspace is None or workspace.numel() < wsb:
-        workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=q.device)
+        workspace = _scratch(max(wsb, 1), q.device, stream)
     _check(_lib.adaspa_block_sparse_attn(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(row_ptr),
                                          _ptr(col_idx), _ptr(o), _ptr(lse), _ptr(workspace), workspace.numel(),
                                          _stream(stream)), "adaspa_block_sparse_attn")
