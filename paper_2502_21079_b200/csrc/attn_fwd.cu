@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       // valid columns: [0, limA) of kv half 0 and [64, limB) of kv half 1 (absolute, 0..128); read
-      // (volatile: issued before the TMEM load, not sunk behind it into the MUFU-congested MIO queue)
+      // (volatile) before the TMEM load, used only before the exponentials
       const int limA = *reinterpret_cast<const volatile int*>(&inf.lim[hq * 2 + 0]);
       const int limB = *reinterpret_cast<const volatile int*>(&inf.lim[hq * 2 + 1]);
       uint32_t s[64];
@@ -595,14 +595,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_wait32(s);
       reg_fence32(s + 32);
       ADASPA_TRACE_EV(1);
-      if (limA < 64 || limB < 128) {  // partial tile / unneeded half: those columns -> -inf
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          const int col = 8 * (i >> 2) + 2 * qd + (i & 1);
-          const int lim = col < 64 ? limA : limB;
-          s[i] = col < lim ? s[i] : __float_as_uint(-INFINITY);
-        }
-      }
+      // The running max is taken over the UNMASKED tile: any m >= the row max of the kept columns is
+      // a valid reference (exact, the final normalisation uses the same m; P of kept keys stays far
+      // above bf16/fp32 underflow), and it keeps the column limits -- a shared-memory load queued
+      // behind MUFU work in MIO, 4.8% of K1's stall samples when it gated the max -- off the
+      // critical path.  The limits are applied below, before the exponentials.
       float mxa[2], mxb[2];  // two partial maxima per row
       mxa[0] = fmaxf(__uint_as_float(s[0]), __uint_as_float(s[1]));
       mxb[0] = fmaxf(__uint_as_float(s[4]), __uint_as_float(s[5]));
@@ -638,6 +635,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mb[0] = (m_used[0] == -INFINITY) ? 0.0f : m_used[0];
       mb[1] = (m_used[1] == -INFINITY) ? 0.0f : m_used[1];
+      if (limA < 64 || limB < 128) {  // partial tile / unneeded half: those columns -> -inf (P = 0)
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const int col = 8 * (i >> 2) + 2 * qd + (i & 1);
+          const int lim = col < 64 ? limA : limB;
+          s[i] = col < lim ? s[i] : __float_as_uint(-INFINITY);
+        }
+      }
       ADASPA_TRACE_EV(2);
       if (__any_sync(0xffffffffu, rescale)) {  // rare: the running max grew by more than 2^8
 #pragma unroll 1
