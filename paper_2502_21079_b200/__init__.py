@@ -7,7 +7,8 @@ The four C-ABI entry points of include/adaspa.h, bound through ctypes:
     select_blocks      K3  head-adaptive hierarchical selection -> CSR
     block_sparse_attn  K4  block-sparse attention forward
 
-plus the host schedule (schedule.py) and head sharding / Ulysses exchange (dist.py).
+plus the host schedule (schedule.py), the paper's plug-and-play `adaspa_attention_handler`
+(handler.py) and head sharding / Ulysses exchange (dist.py).
 Importing fails loudly if libadaspa.so was not built: there is no CPU fallback.
 """
 
@@ -16,3 +17,4 @@ from ._lib import (  # noqa: F401
     select_blocks, block_sparse_attn, sparse_workspace_bytes, SELECT_RECALL, SELECT_SPARSITY,
     FLAG_TEXT_SINK, FLAG_HEAD_TIERS, LIB_PATH,
 )
+from .handler import AdaSpaAttentionHandler, adaspa_attention_handler  # noqa: F401,E402
