@@ -231,6 +231,40 @@ def test_block_sparse_attn_large_nb(ada):
         compare_out(o[0, 0, r], ro, lse[0, 0, r], rl, what=f"large-nb K4 qb{p}")
 
 
+@pytest.mark.parametrize("tf,block,d", [(False, 128, 128), (True, 64, 64), (True, 128, 64), (False, 64, 128)])
+def test_hot_path_batch2(ada, tf, block, d):
+    """K1 -> K2 -> K3 -> K4 through HotPath at batch 2 (per-(b,h) items, row offsets and the
+    per-batch head tiers of K3 span both batch elements): every head of both batch elements against
+    the oracle pipeline (K2 with the GPU's LSE; K4 on the GPU's CSR)."""
+    from paper_2502_21079_b200.hotpath import HotPath
+    lay = _lay("tiny_tf" if tf else "tiny", dict(f=4, h=9, w=10, n_text=45, head_dim=d, block=block, heads=3))
+    q, k, v = _qkv(lay, batch=2)
+    hp = HotPath(2, lay.heads, lay.n, lay.head_dim, lay.block, lay.n_text, lay.text_first, targets=0.9)
+    o = hp.run(q, k, v)
+    torch.cuda.synchronize()
+    blocks = oracle.block_map(lay.n_video, lay.n_text, lay.block, lay.text_first)
+    nb = len(blocks)
+    scale = 1 / math.sqrt(lay.head_dim)
+    rows = csr_rows(hp.csr.row_ptr, hp.csr.col_idx)
+    for b in range(2):
+        for h in range(lay.heads):
+            qq, kk, vv = np64(q[b, h]), np64(k[b, h]), np64(v[b, h])
+            od, lse = oracle.dense_attention(qq, kk, vv, scale)
+            compare_out(hp.o_dense[b, h], od, hp.lse[b, h], lse, what=f"b{b} h{h} K1")
+            M = oracle.block_mass(qq, kk, hp.lse[b, h].double().cpu().numpy(), blocks, scale)
+            Mg = hp.mass[b, h].double().cpu().numpy()
+            L = np.array([bl.length for bl in blocks], dtype=np.float64)[:, None]
+            assert (np.abs(Mg - M) / L).max() <= MASS_REL, f"b{b} h{h} K2"
+            for p in range(nb):
+                forced, cands = oracle.row_forced_and_candidates(blocks, p, True)
+                ok = oracle.select_row_recall(M[p], forced, cands, 0.9)
+                good, msg = selection_ok(M[p], forced, cands, 0.9, rows[(b * lay.heads + h) * nb + p], ok)
+                assert good, f"b{b} h{h} row {p}: {msg}"
+            kept = [rows[(b * lay.heads + h) * nb + p] for p in range(nb)]
+            so, _ = oracle.masked_attention(qq, kk, vv, blocks, kept, scale)
+            compare_out(o[b, h], so, what=f"b{b} h{h} K4")
+
+
 def test_end_to_end_tiny(ada):
     """K1 -> K2 (fresh LSE) -> K3 (recall 0.9) -> K4 against the oracle pipeline, both text orders."""
     for name in ("tiny", "tiny_tf"):
