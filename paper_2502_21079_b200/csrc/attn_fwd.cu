@@ -66,6 +66,12 @@ namespace {
 constexpr int kThreads = 640;
 __device__ __forceinline__ uint32_t s_col(int t) { return static_cast<uint32_t>(t) * 128u; }
 __device__ __forceinline__ uint32_t o_col(int t) { return 256u + static_cast<uint32_t>(t) * 128u; }
+// d=64: O_t uses 64 of its 128 columns, so P_t gets the other 64 instead of aliasing S_t.  The next
+// QK_t then only waits for the softmax to have LOADED S_t, not for PV_t: no softmax -> PV -> QK
+// chain, and the kernel is bound by exponential throughput (at d=64 MUFU work is twice the MMA
+// work).  d=128 has no spare TMEM and keeps P in S (the chain stays).
+template <int D>
+__device__ __forceinline__ uint32_t p_col(int t) { return D == 64 ? o_col(t) + 64u : s_col(t); }
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef ADASPA_EXP_POLY_MOD
 #define ADASPA_EXP_POLY_MOD 8
@@ -112,6 +118,7 @@ struct Bars {
   uint64_t kv_full[12], kv_empty[12];
   uint64_t q_full, q_empty;
   uint64_t s_full[2], p_half[2], p_full[2], o_full[2], o_empty[2];
+  uint64_t s_loaded[2], p_free[2];  // d=64 only: S_t in registers / PV_t done (P_t may be overwritten)
   SlotMeta meta[12];
   TileInfo info[2][2];
   ItemInfo qitem;
@@ -169,6 +176,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap tv, const AttnParams p) {
   using S = Smem<D>;
   constexpr int NS = S::kNS;
+  constexpr bool kSepP = D == 64;
+  // d=64: one MMA issuer per q tile (warps 1 and 3), the two tiles' chains are independent (P has
+  // its own TMEM columns).  d=128: one issuer for both, whose PV0, QK0, PV1, QK1 order interleaves
+  // the two chains on the tensor pipe (measured: two issuers there cost 13%).
+  constexpr int kIssuers = kSepP ? 2 : 1;
   constexpr int TILE = S::kTile;
   constexpr int CH = D / 64;            // 64-column (128-byte) chunks per row
   constexpr int CHUNK = 128 * 128;      // bytes per chunk of a 128-row tile
@@ -184,14 +196,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&bars->kv_full[i], 1);
-      mbar_init(&bars->kv_empty[i], 1);
+      mbar_init(&bars->kv_empty[i], kIssuers);  // one release per MMA issuer
     }
     mbar_init(&bars->q_full, 1);
-    mbar_init(&bars->q_empty, 1);
+    mbar_init(&bars->q_empty, kIssuers);
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bars->s_full[t], 2);
       mbar_init(&bars->p_half[t], 8);  // P columns [0, 32) (kv rows 0-63) of every row stored
       mbar_init(&bars->p_full[t], 8);
+      mbar_init(&bars->s_loaded[t], 8);
+      mbar_init(&bars->p_free[t], 1);
       mbar_init(&bars->o_full[t], 1);
       mbar_init(&bars->o_empty[t], 8);
     }
@@ -303,16 +317,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       bars->meta[slot].kind = kAllEnd;
       mbar_arrive(&bars->kv_full[slot]);
     }
-  } else if (warp == 1) {
-    // ============================================================ MMA issuer
+  } else if (warp == 1 || (kIssuers == 2 && warp == 3)) {
+    // ============================================================ MMA issuer(s)
+    // kIssuers == 2: one issuer thread per q tile (warp 1: tile 0, warp 3: tile 1), each following
+    // the same K/V ring, so a wait for one tile's P never holds back the other tile's MMAs; K/V
+    // slots and Q are released after both issuers' commits (count-2 barriers).  T = -1: both tiles.
     if (lane == 0) {
+      const int T = kIssuers == 1 ? -1 : (warp == 1 ? 0 : 1);
       constexpr uint32_t kIdescQK = idesc_bf16(128, 128, false, false);
       constexpr uint32_t kIdescPV = idesc_bf16(128, D, false, true);
       const uint32_t sq_addr = smem_u32(sQ);
       const uint32_t skv_addr = smem_u32(sKV);
       int slot = 0;
       uint32_t ph = 0, qph = 0;
-      uint32_t pph[2] = {0u, 0u}, oeph[2] = {0u, 0u};
+      uint32_t pph[2] = {0u, 0u}, oeph[2] = {0u, 0u}, slph[2] = {0u, 0u};
+      bool slp[2] = {false, false};  // kSepP: an S_t whose s_loaded arrival is not consumed yet
+      auto wait_loaded = [&](int t) {
+        if (!kSepP || !slp[t]) return;
+        mbar_wait(&bars->s_loaded[t], slph[t]);
+        slph[t] ^= 1;
+        slp[t] = false;
+        tc_fence_after();
+      };
       int icnt[2] = {0, 0};
       bool o_dirty[2] = {false, false};
       int tr_n = 0;
@@ -334,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k4 = 0; k4 < 4; ++k4) {
           const int kk = 4 * half + k4;
           const uint64_t b = desc_sw128(skv_addr + vslot * TILE + kk * 2048, CHUNK, 1024);
-          mma_ts(tmem + o_col(t), tmem + s_col(t) + kk * 8, b, kIdescPV, (first && kk == 0) ? 0u : 1u);
+          mma_ts(tmem + o_col(t), tmem + p_col<D>(t) + kk * 8, b, kIdescPV, (first && kk == 0) ? 0u : 1u);
         }
       };
       // wait for P_t (both halves) and issue PV_t; O must have been drained by the epilogue first
@@ -352,6 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         pph[t] ^= 1;
         tc_fence_after();
         issue_pv_half(t, vslot, false, 1);
+        if (kSepP) tc_commit(&bars->p_free[t]);
       };
 
       for (;;) {
@@ -361,6 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (mt.kind == kAllEnd) {
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
+            if (T >= 0 && t != T) continue;
             bars->info[t][icnt[t] & 1].kind = kAllEnd;
             ++icnt[t];
             mbar_arrive_n(&bars->s_full[t], 2);
@@ -384,7 +412,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
+              if (T >= 0 && t != T) continue;
               if (!pend[t]) continue;
+              wait_loaded(t);
               wait_issue_pv(t, pvslot, first_pv[t]);
               first_pv[t] = false;
             }
@@ -392,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_commit(&bars->q_empty);
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
+              if (T >= 0 && t != T) continue;
               if (had[t]) {
                 tc_commit(&bars->o_full[t]);
                 o_dirty[t] = true;
@@ -420,21 +451,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++slot == NS) { slot = 0; ph ^= 1; }
           if (pvslot >= 0) {
             mbar_wait(&bars->kv_full[pvslot], pvph);
-            ADASPA_TRACE_MMA(4);
+            if (T <= 0) ADASPA_TRACE_MMA(4);
             tc_fence_after();
+          }
+          // kSepP (d=64): this entry's QKs go first (they only need the previous S_t loaded), then
+          // the previous entry's PVs.  Otherwise PV_t(prev) must precede QK_t (P_t aliases S_t).
+          bool pv_pend[2] = {pend[0], pend[1]};
+          if (kSepP) {
+#pragma unroll
+            for (int t = 0; t < 2; ++t) pend[t] = false;
           }
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
-            if (pend[t]) {
+            if (T >= 0 && t != T) continue;
+            if (!kSepP && pv_pend[t]) {
               wait_issue_pv(t, pvslot, first_pv[t]);
-              ADASPA_TRACE_MMA(t * 2 + 0);
+              if (T <= 0) ADASPA_TRACE_MMA(t * 2 + 0);
               first_pv[t] = false;
               pend[t] = false;
             }
             const uint32_t need = (static_cast<uint32_t>(mt.mask) >> (4 * t)) & 0xFu;
             if (need) {
+              wait_loaded(t);
               issue_qk(t, kslot);
-              ADASPA_TRACE_MMA(t * 2 + 1);
+              if (kSepP) slp[t] = true;
+              if (T <= 0) ADASPA_TRACE_MMA(t * 2 + 1);
               TileInfo& inf = bars->info[t][icnt[t] & 1];
               ++icnt[t];
               inf.kind = kNormal;
@@ -455,12 +496,24 @@ __global__ void __launch_bounds__(kThreads, 1)
               had[t] = true;
             }
           }
+          if (kSepP) {
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              if (T >= 0 && t != T) continue;
+              if (!pv_pend[t]) continue;
+              // a tile that skipped this entry still has its S loaded-arrival outstanding
+              if (!((static_cast<uint32_t>(mt.mask) >> (4 * t)) & 0xFu)) wait_loaded(t);
+              wait_issue_pv(t, pvslot, first_pv[t]);
+              if (T <= 0) ADASPA_TRACE_MMA(t * 2 + 0);
+              first_pv[t] = false;
+            }
+          }
           if (pvslot >= 0) tc_commit(&bars->kv_empty[pvslot]);
           tc_commit(&bars->kv_empty[kslot]);
           pvslot = vslot;
           pvph = vph;
           mbar_wait(&bars->kv_full[slot], ph);
-          ADASPA_TRACE_MMA(5);
+          if (T <= 0) ADASPA_TRACE_MMA(5);
           tc_fence_after();
           mt = bars->meta[slot];
         }
@@ -487,6 +540,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32 + hh * 16) << 16;
     const uint32_t s_addr = tmem + lane_base + s_col(t);
     const uint32_t o_addr = tmem + lane_base + o_col(t);
+    const uint32_t p_addr = tmem + lane_base + p_col<D>(t);
+    uint32_t pfph = 0;
+    int pcnt = 0;  // kSepP: normal tiles processed; the n-th (n >= 1) waits for PV of the (n-1)-th
+    auto wait_p_free = [&]() {
+      if (!kSepP || pcnt == 0) return;
+      mbar_wait(&bars->p_free[t], pfph);
+      pfph ^= 1;
+      tc_fence_after();
+    };
     const float sl2 = p.scale_log2;
     uint32_t sph = 0, oph = 0;
     int icnt = 0;
@@ -579,6 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         ADASPA_TRACE_EV(3);
         if (lane == 0) {
+          if (kSepP) mbar_arrive(&bars->s_loaded[t]);
           mbar_arrive(&bars->p_half[t]);
           mbar_arrive(&bars->p_full[t]);
         }
@@ -594,6 +657,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_16x256b_x8(s_addr + 64, s + 32);
       tmem_ld_wait32(s);
       reg_fence32(s + 32);
+      if (kSepP) {  // S_t is in registers: the next QK_t may overwrite it
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->s_loaded[t]);
+      }
       ADASPA_TRACE_EV(1);
       // The running max is taken over the UNMASKED tile: any m >= the row max of the kept columns is
       // a valid reference (exact, the final normalisation uses the same m; P of kept keys stays far
@@ -644,6 +712,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       ADASPA_TRACE_EV(2);
+      wait_p_free();  // kSepP: PV of the previous tile has read P_t and accumulated into O_t
+      ++pcnt;
       if (__any_sync(0xffffffffu, rescale)) {  // rare: the running max grew by more than 2^8
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
@@ -685,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk[2 * k] = pack_bf16x2(p0.x, p0.y);
           pk[2 * k + 1] = pack_bf16x2(p1.x, p1.y);
         }
-        tmem_st_16x128b_x8(s_addr + c * 32, pk);
+        tmem_st_16x128b_x8(p_addr + c * 32, pk);
         if (c == 0) {  // first half of P stored: the MMA thread may start PV on kv rows 0-63
           tmem_st_wait();
           tc_fence_before();
