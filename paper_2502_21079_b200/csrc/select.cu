@@ -82,16 +82,14 @@ __global__ void __launch_bounds__(256, KPL <= 32 ? 3 : 1) select_rows_kernel(Sel
   const int t0 = p.text_first ? 0 : p.grid.nb_first;
   const int t1 = p.text_first ? p.grid.nb_first : nb;
 
-  // element i of this lane is kv-block j = 32 i + lane (KPL is up to 128 elements per lane, so the
-  // candidate / forced status is recomputed from j rather than kept in a 32-bit mask)
-  auto is_forced = [&](int i) -> bool {
-    const int j = i * 32 + lane;
-    return j < nb && p.text_sink && j >= t0 && j < t1;
-  };
-  auto is_cand = [&](int i) -> bool {
-    const int j = i * 32 + lane;
-    return j < nb && !(p.text_sink && j >= t0 && j < t1);
-  };
+  // element i of this lane is kv-block j = 32 i + lane; candidate / forced bits per element in
+  // ceil(KPL/32) words (KPL reaches 192 elements per lane; a single 32-bit mask overflowed)
+  constexpr int KW = (KPL + 31) / 32;
+  uint32_t cmask[KW], fmask[KW];
+#pragma unroll
+  for (int w = 0; w < KW; ++w) cmask[w] = fmask[w] = 0u;
+  auto is_cand = [&](int i) -> bool { return (cmask[i >> 5] >> (i & 31)) & 1u; };
+  auto is_forced = [&](int i) -> bool { return (fmask[i >> 5] >> (i & 31)) & 1u; };
   float m[KPL];
   int ncand_l = 0, nforced_l = 0;
   double tsum = 0.0, fsum = 0.0;
@@ -100,12 +98,15 @@ __global__ void __launch_bounds__(256, KPL <= 32 ? 3 : 1) select_rows_kernel(Sel
     const int j = i * 32 + lane;
     const bool valid = j < nb;
     const float x = valid ? __ldg(mrow + j) : 0.0f;
-    const bool forced = is_forced(i);
+    const bool forced = valid && p.text_sink && j >= t0 && j < t1;
+    const bool cand = valid && !forced;
     tsum += f2d_volatile(x);
     if (forced) fsum += f2d_volatile(x);
-    ncand_l += is_cand(i) ? 1 : 0;
+    cmask[i >> 5] |= cand ? (1u << (i & 31)) : 0u;
+    fmask[i >> 5] |= forced ? (1u << (i & 31)) : 0u;
+    ncand_l += cand ? 1 : 0;
     nforced_l += forced ? 1 : 0;
-    m[i] = is_cand(i) ? x : 0.0f;  // candidate masses only (forced mass is F)
+    m[i] = cand ? x : 0.0f;  // candidate masses only (forced mass is F)
   }
   const double T = warp_sum_f64(tsum);
   const double F = warp_sum_f64(fsum);
