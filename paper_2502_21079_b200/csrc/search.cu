@@ -154,10 +154,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&bars->kv_full[i], 1);
-      mbar_init(&bars->kv_empty[i], 1);
+      mbar_init(&bars->kv_empty[i], 2);  // one release per MMA issuer (one per q tile)
     }
     mbar_init(&bars->q_full, 1);
-    mbar_init(&bars->q_empty, 1);
+    mbar_init(&bars->q_empty, 2);
     for (int t = 0; t < 2; ++t)
       for (int b = 0; b < 2; ++b) {
         mbar_init(&bars->s_full[t][b], 1);
@@ -214,8 +214,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || warp == 3) {
+    // one MMA issuer per q tile (warp 1: tile 0, warp 3: tile 1): a tile whose exp warps lag
+    // does not hold back the other tile's QK^T; K slots and Q are released by both (count 2)
     if (lane == 0) {
+      const int T = warp == 1 ? 0 : 1;
       constexpr uint32_t kIdesc = idesc_bf16(128, 128, false, false);
       const uint32_t sq_addr = smem_u32(sQ);
       const uint32_t sk_addr = smem_u32(sK);
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const int buf = j & 1;
           for (int t = 0; t < 2; ++t) {
-            if (!q.exists[t]) continue;
+            if (t != T || !q.exists[t]) continue;
             mbar_wait(&bars->s_empty[t][buf], seph[t][buf] ^ 1);
             seph[t][buf] ^= 1;
             tc_fence_after();
