@@ -104,7 +104,6 @@ struct ItemInfo {
 template <int D>
 struct Smem {
   static constexpr int kTile = 128 * D * 2;  // one 128-row tile of d bf16 columns
-  // ADASPA_ABLATE 5 (diagnostic): one shared Q tile, 5 K/V slots -- pipeline depth experiment
   // d=128: Q (64 KB) + 5 K/V slots (160 KB) + barriers fill the 227 KB; 5 slots let the producer
   // run ~2.5 entries ahead (with 4, the MMA thread waited ~280 cycles per entry for the next K).
   static constexpr int kNS = (D == 128) ? 5 : 10;

@@ -47,6 +47,9 @@ __device__ unsigned long long g_ptrace[3][4096];
 
 namespace {
 
+#ifndef ADASPA_ABLATE
+#define ADASPA_ABLATE 0  // diagnostic builds only: 4 = no softmax, 6 = softmax TMEM traffic only
+#endif
 constexpr int kThreads = 384;
 constexpr int kD = 128;
 constexpr int kTileQ = 128 * kD * 2;  // 32 KB: two 64-column chunks of 16 KB
@@ -435,9 +438,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int skip = vinf->skip, last = vinf->last;
       const int limA = vinf->lim0, limB = vinf->lim1;
       const uint32_t s_addr = tmem + lane_base + 128u * b;
-#ifndef ADASPA_ABLATE
-#define ADASPA_ABLATE 0
-#endif
       if (ADASPA_ABLATE == 4) {  // diagnostic: no softmax (MMA / TMA pipeline alone)
       } else if (ADASPA_ABLATE == 6) {  // diagnostic: the softmax's TMEM traffic only (P = 0)
         uint32_t s[64];
