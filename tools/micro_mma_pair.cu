@@ -32,6 +32,27 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int iters, unsigned long lo
     constexpr uint32_t id_ts = idesc_bf16(M, 128, false, true);
     unsigned long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
+      if (MODE == 7 || MODE == 8) {  // one 128-row kv tile of attention at d=128, one q tile
+        // 7: QK as 8 SS N=128 + PV as 8 TS N=128 (P aliased in S)
+        // 8: two 64-row half steps, each 8 SS N=64 (QK) + 4 TS N=128 (PV, K=64)
+        constexpr uint32_t id64 = idesc_bf16(128, 64, false, false);
+#pragma unroll
+        for (int hs = 0; hs < (MODE == 7 ? 1 : 2); ++hs) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            const uint64_t ad = desc_sw128(a + off, 16, 1024), bd = desc_sw128(b + off + hs * 8192, 16, 1024);
+            if (MODE == 7) mma_ss(tmem, ad, bd, id_ss, 1u);
+            else mma_ss(tmem + 64 * hs, ad, bd, id64, 1u);
+          }
+#pragma unroll
+          for (int kk = 0; kk < (MODE == 7 ? 8 : 4); ++kk) {
+            const uint64_t bv = desc_sw128(b + (hs * 4 + kk) * 2048, 16384, 1024);
+            mma_ts(tmem + 384, tmem + 128 + (hs * 4 + kk) * 8, bv, id_ts, 1u);
+          }
+        }
+        continue;
+      }
       if (MODE == 6) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -104,7 +125,7 @@ void run(const char* name, int grid, unsigned long long* d) {
   cudaMemcpy(h, d, 8 * grid, cudaMemcpyDeviceToHost);
   unsigned long long mx = 0;
   for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
-  const int per_iter = MODE >= 2 ? 16 : 8;
+  const int per_iter = MODE >= 2 ? 16 : 8;  // modes 7/8: per 16 N=128-equivalent MMAs
   printf("%-34s grid %3d %s  cycles/MMA = %.1f\n", name, grid, cudaGetErrorString(e), (double)mx / (iters * per_iter));
 }
 
@@ -124,6 +145,8 @@ int main() {
     run<5, true>("pair 8 SS, drain, 8 TS", grid, d);
     run<6, true>("pair (TS,SS) x8 interleaved, drain", grid, d);
     run<5, false>("1SM 8 SS, drain, 8 TS", grid, d);
+    run<7, false>("1SM kv tile: 8 SS128 + 8 TS", grid, d);
+    run<8, false>("1SM kv tile: 2x(8 SS64 + 4 TS)", grid, d);
   }
   return 0;
 }
