@@ -265,6 +265,40 @@ def test_hot_path_batch2(ada, tf, block, d):
             compare_out(o[b, h], so, what=f"b{b} h{h} K4")
 
 
+@pytest.mark.parametrize("block,d,tf", [(128, 128, False), (64, 128, True), (64, 64, False)])
+def test_block_sparse_attn_midsize_random(ada, block, d, tf):
+    """K4 with many work items per head (N = 16.5K tokens, H = 3: hundreds of items through the
+    dynamic queue in LPT order) on a random CSR with ragged row lengths (1 to ~40% of the blocks,
+    plus rows that keep every block); sampled q-blocks of every head against the oracle."""
+    lay = _lay("tiny_tf" if tf else "tiny", dict(f=8, h=16, w=128, n_text=77, head_dim=d, block=block, heads=3))
+    q, k, v = _qkv(lay)
+    blocks = oracle.block_map(lay.n_video, lay.n_text, lay.block, lay.text_first)
+    nb = len(blocks)
+    g = np.random.default_rng(block + d)
+    rows = []
+    for r in range(lay.heads * nb):
+        kind = g.random()
+        if kind < 0.05:
+            ids = list(range(nb))
+        else:
+            n = int(g.integers(1, max(2, int(0.4 * nb))))
+            ids = sorted(g.choice(nb, n, replace=False).tolist())
+        rows.append(ids)
+    rp = torch.tensor(np.cumsum([0] + [len(r) for r in rows]), dtype=torch.int32, device="cuda")
+    ci = torch.tensor([j for r in rows for j in r], dtype=torch.int32, device="cuda")
+    o, lse = ada.block_sparse_attn(q, k, v, rp, ci, block_size=lay.block, n_text=lay.n_text,
+                                   text_first=lay.text_first, want_lse=True)
+    torch.cuda.synchronize()
+    scale = 1 / math.sqrt(lay.head_dim)
+    for h in range(lay.heads):
+        qh, kh, vh = np64(q[0, h]), np64(k[0, h]), np64(v[0, h])
+        for p in sorted({0, nb - 1, *g.choice(nb, 12, replace=False).tolist()}):
+            b = blocks[p]
+            r = slice(b.start, b.start + b.length)
+            ro, rl = oracle.masked_attention(qh, kh, vh, blocks, {p: rows[h * nb + p]}, scale, q_block_ids=[p])
+            compare_out(o[0, h, r], ro, lse[0, h, r], rl, what=f"mid B{block} d{d} h{h} qb{p}")
+
+
 def test_end_to_end_tiny(ada):
     """K1 -> K2 (fresh LSE) -> K3 (recall 0.9) -> K4 against the oracle pipeline, both text orders."""
     for name in ("tiny", "tiny_tf"):
