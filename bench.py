@@ -234,14 +234,11 @@ def run_ours(args):
     kfl, nnz = kept_flops(lay, hp.csr, lay.head_dim)
     nb = hp.nb
     H, N, d = lay.heads, lay.n, lay.head_dim
-    t = torch.tensor([total, tk[3], tk[0], tk[1], tk[2]], dtype=torch.float64, device=dev)
-    work = torch.tensor([kfl], dtype=torch.float64, device=dev)
-    if ws > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(work, op=torch.distributed.ReduceOp.SUM)
-    total_max, k4_max = float(t[0]), float(t[1])
+    from paper_2502_21079_b200.dist import reduce_step_timings
     K = args.steps
-    value = work.item() * K / (k4_max / 1e3) / 1e12
+    value, tmax = reduce_step_timings([total, tk[0], tk[1], tk[2], tk[3]], kfl, K)  # max over ranks
+    total_max, k4_max = tmax[0], tmax[4]
+    work = torch.tensor([value * (k4_max / 1e3) * 1e12 / K], dtype=torch.float64)  # sum over ranks
 
     # e2e: the same metric (K4 TFLOP/s on kept blocks) for a sparse step end to end through the public
     # API from pinned host buffers: H2D of Q,K,V, the block-sparse forward on the cached CSR, D2H of O,

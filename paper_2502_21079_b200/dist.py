@@ -88,3 +88,20 @@ def ulysses_out(o_heads, n_local_sizes, group=None):
 def as_bhnd(x_nhd):
     """[N, Hp, d] token-major -> a [1, Hp, N, d] strided view (stride_n = Hp*d, stride_h = d)."""
     return x_nhd.permute(1, 0, 2).unsqueeze(0)
+
+
+def reduce_step_timings(kernel_ms, kept_flops, steps, group=None):
+    """Whole-job numbers of a weak-scaling bench run (bench.py): every rank timed
+    `steps` steps of its own layer; kernel_ms = [total, K1, K2, K3, K4] summed over the steps (ms).
+    Returns (value TFLOP/s = sum over ranks of kept FLOPs x steps / the slowest rank's K4 time,
+    per-kernel max-over-ranks ms).  Single process: no collective."""
+    t = torch.tensor([float(x) for x in kernel_ms], dtype=torch.float64)
+    w = torch.tensor([float(kept_flops)], dtype=torch.float64)
+    if dist.is_available() and dist.is_initialized():
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else t.device
+        t, w = t.to(dev), w.to(dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        dist.all_reduce(w, op=dist.ReduceOp.SUM, group=group)
+    t = t.cpu()
+    value = float(w.item()) * steps / (float(t[4]) / 1e3) / 1e12
+    return value, [float(x) for x in t]

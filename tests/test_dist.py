@@ -77,3 +77,39 @@ def test_lpt_assign():
     loads = [sum(costs[h] for h in p) for p in parts]
     assert max(loads) - min(loads) <= max(costs)
     assert max(loads) <= sum(costs) / 3 + max(costs)
+
+
+def _timing_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank r: total, K1..K4 ms over 5 steps; kept FLOPs of its own layer
+        ms = [100.0 + rank, 50.0 + 3 * rank, 30.0, 0.2, 10.0 + 2 * rank]
+        value, tmax = D.reduce_step_timings(ms, 1e12 * (rank + 1), 5)
+        q.put((rank, value, tmax))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_reduce_step_timings_gloo():
+    """bench.py's whole-job aggregation at world size 2: times are the max over ranks (per kernel),
+    the work is the sum; value = sum(kept FLOPs) x steps / slowest K4 time."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_timing_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want_t = [101.0, 53.0, 30.0, 0.2, 12.0]
+    want_v = (1e12 + 2e12) * 5 / (12.0 / 1e3) / 1e12
+    for _, value, tmax in res:
+        assert tmax == pytest.approx(want_t)
+        assert value == pytest.approx(want_v)
+    v1, t1 = D.reduce_step_timings([1.0, 2.0, 3.0, 4.0, 5.0], 2e12, 2)  # single process
+    assert t1 == [1.0, 2.0, 3.0, 4.0, 5.0] and v1 == pytest.approx(2e12 * 2 / 5e-3 / 1e12)
