@@ -20,3 +20,13 @@ def test_pair_kernel_matches_oracle(case):
                        env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "pair ok" in r.stdout
+
+
+def test_pair_kernel_rescale_path():
+    """The pair kernel's O-rescale path (pv_done barriers) on the ramped-logit workload of
+    tests/test_gpu_rescale.py (d = 128, block 128: the shapes the pair kernel serves)."""
+    env = dict(os.environ, ADASPA_PAIR="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_rescale.py"),
+                        "-m", "gpu", "-q", "-p", "no:cacheprovider", "-k", "128-128"],
+                       env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0 and "1 passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
