@@ -169,6 +169,35 @@ def test_select_blocks_exact_large_nb(ada, nv, nt, mode):
             assert got == exp, f"nb={nb} {mode} h{h} row {p}: {len(got)} kept vs {len(exp)} (first {got[:6]} / {exp[:6]})"
 
 
+@pytest.mark.parametrize("mode", ["recall", "sparsity"])
+def test_select_blocks_zero_masses(ada, mode):
+    """K3 on rows where most candidate masses are exactly 0 (fp32 underflow of far blocks in sharp
+    heads): SPARSITY budgets larger than the non-zero count must take zero-mass blocks in ascending
+    id order (reading R10), RECALL must stop at the non-zero prefix; all-zero rows keep the forced
+    set / the first candidate (R25).  Bit-exact against the oracle on identical masses."""
+    H, nv, nt, B = 3, 3000, 150, 64
+    blocks = oracle.block_map(nv, nt, B, False)
+    nb = len(blocks)
+    Mt = workloads.random_masses(H * nb, nb, seed=9).view(1, H, nb, nb).clone()
+    g = torch.Generator().manual_seed(4)
+    zero = torch.rand(1, H, nb, nb, generator=g) < 0.9
+    Mt[zero] = 0.0
+    Mt[0, 1, 5] = 0.0   # one all-zero row
+    q = torch.empty(1, H, nv + nt, 64, dtype=torch.bfloat16, device="cuda")
+    desc = ada.make_desc(q, B, nt, False)
+    targets = [0.9, 0.5, 0.99] if mode == "recall" else [0.5, 0.8, 0.95]
+    kmode = ada.SELECT_RECALL if mode == "recall" else ada.SELECT_SPARSITY
+    out = ada.select_blocks(Mt.cuda(), heads_desc=desc, mode=kmode, target=targets, flags=1)
+    torch.cuda.synchronize()
+    M64 = Mt[0].double().numpy()
+    keep, _, _, _ = oracle.select_blocks(M64, blocks, mode, targets, text_sink=True)
+    rows = csr_rows(out.row_ptr, out.col_idx)
+    for h in range(H):
+        for p in range(nb):
+            exp = np.nonzero(keep[h, p])[0].tolist()
+            assert rows[h * nb + p] == exp, f"{mode} h{h} row {p}: {rows[h * nb + p][:8]} vs {exp[:8]}"
+
+
 def _random_csr(H, nb, density, seed):
     g = np.random.default_rng(seed)
     keep = g.random((H, nb, nb)) < density
