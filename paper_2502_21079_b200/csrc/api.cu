@@ -155,6 +155,16 @@ bool use_pair(const adaspa_attn_desc* d, bool sparse) {
   return enabled && d->head_dim == 128 && (!sparse || d->block_size == 128);
 }
 
+// d = 128 dense pass with one q tile per SM and two alternating softmax groups (attn_one.cu);
+// opt-in (ADASPA_ONE=1) until it beats attn_fwd.cu.
+bool use_one(const adaspa_attn_desc* d) {
+  static const bool enabled = [] {
+    const char* e = getenv("ADASPA_ONE");
+    return e && e[0] >= '1' && e[0] <= '4';  // 2-4: diagnostic ablations (attn_one.cu)
+  }();
+  return enabled && d->head_dim == 128;
+}
+
 struct SparseWs {
   int items_per_bh, num_items, stride;
   size_t queue, len, order, stream, bytes;
@@ -225,6 +235,7 @@ adaspa_status adaspa_dense_attn_lse(const adaspa_attn_desc* desc, const void* q,
   p.items_per_bh = (desc->seq_len + 255) / 256;
   p.num_items = desc->batch * desc->heads * p.items_per_bh;
   cudaError_t e = pair ? launch_attn_pair(tq, tk, tv, p, false, num_sms(), (cudaStream_t)stream)
+                 : use_one(desc) ? launch_attn_one(tq, tk, tv, p, num_sms(), (cudaStream_t)stream)
                        : launch_attn(tq, tk, tv, p, desc->head_dim, false, false, num_sms(), (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "dense_attn_lse launch");
   return ADASPA_OK;
