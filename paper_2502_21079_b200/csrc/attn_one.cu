@@ -267,8 +267,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
     const int hh = (wi >> 2) & 1;
     const int wq = warp & 3;
     const int qd = lane & 3;
-    const int rw0 = hh * 16 + (lane >> 2);  // row within the warp's lane quarter... (absolute below)
-    const int row0 = wq * 32 + rw0;
+    const int row0 = wq * 32 + hh * 16 + (lane >> 2);  // tile rows of this thread: row0, row0 + 8
     const int row1 = row0 + 8;
     const int rloc = lane >> 2;  // row index within the warp's 16 rows (row0 -> rloc, row1 -> rloc + 8)
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32 + hh * 16) << 16;
