@@ -266,7 +266,7 @@ def run_ours(args):
                "d2h_bytes_per_step": q.numel() * q.element_size(),
                "ms_per_step": round(te.item() / K, 3),
                "note": "sparse step from pinned host memory: H2D Q,K,V + K4 (cached CSR) + D2H O, "
-                       "overlapped over 12 head groups (tools/e2e_groups.py: 4 -> 49.9 ms, 12 -> 44.9 ms, bound: 37.1 ms of pinned H2D at 55.6 GB/s); TFLOP/s on kept blocks"}
+                       "overlapped over 24 head groups, K4 launches alternating between two compute streams (tools/e2e_groups.py: 12 -> 45.0 ms, 16 -> 44.4 ms, 24 -> 43.8 ms; bound: 37.1 ms of pinned H2D at 55.5 GB/s); TFLOP/s on kept blocks"}
 
     if rank != 0:
         if ws > 1:
