@@ -1,17 +1,23 @@
 #!/usr/bin/env python
-"""bench.py -- AdaSpa hot path on B200 (driver contract; DESIGN.md §7).
+"""bench.py -- AdaSpa hot path on B200 (driver contract; DESIGN.md §7-8).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config hyv110k]
+                    [--lpt] [--ulysses] [--no-variants]
 
 A step is one pass of the whole hot path over one HunyuanVideo-shaped layer
 (BASELINE.json configs[2]: H=24, d=128, ~110K tokens, block 128, head-adaptive recall 0.9):
 K1 dense attention + LSE -> K2 LSE-cached block-mass search -> K3 selection -> K4 block-sparse
 forward.  metric = BASELINE.json's metric; `value` = effective TFLOP/s of the block-sparse forward
 on kept blocks (4*d*sum_kept |qb||kb| / K4 time), whole job: sum over ranks / max over ranks.
-ms/layer, the search overhead and every kernel's roofline are extra keys.
+ms/layer, the search overhead and every kernel's roofline (median / p90 per kernel) are extra keys;
+`variants` holds the paper's default selection (sparsity 0.8 + head tiers) on the same layer and the
+CogVideoX-shaped layer (configs[1]).
 
-Multi-GPU (torchrun): weak scaling -- every rank runs its own layer (its own seed) on its own GPU;
-the path has no exchange step, so there is no data-path collective.
+Multi-GPU (`--gpus N` spawns N ranks through torch.distributed.run unless already under torchrun):
+ONE layer, head-sharded -- strong scaling.  Rank p runs the search on its
+contiguous head group (equal dense work); `--lpt` then all-gathers the CSRs (NCCL, timed as
+`exchange`) and runs K4 on a longest-processing-time head set by kept tiles; `--ulysses` adds the
+sequence->head all-to-all of Q/K/V in and O out (BASELINE configs[3]).
 `--impl reference`: the fp64 oracle (oracle/) timed on the host cores on a bounded sample.
 """
 
@@ -42,13 +48,35 @@ def parse():
     ap.add_argument("--config", default="hyv110k")
     ap.add_argument("--recall", type=float, default=0.9)
     ap.add_argument("--mode", default="recall", choices=["recall", "sparsity-tiers"])
+    ap.add_argument("--lpt", action="store_true",
+                    help="K4 on an LPT head set by kept tiles (CSRs all-gathered after the search)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ulysses", action="store_true",
-                    help="BASELINE configs[3]: one layer, sequence-sharded activations, NCCL all-to-all to "
-                         "head shards, K1..K4 on H/N heads per rank, all-to-all of O back (strong scaling)")
+                    help="BASELINE configs[3]: sequence-sharded activations, NCCL all-to-all to head shards "
+                         "and back around the search step and around the sparse step (strong scaling)")
     return ap.parse_args()
+
+
+def maybe_spawn(args):
+    """`--gpus N` outside torchrun: re-launch this command as N ranks (one per GPU) through
+    torch.distributed.run on 127.0.0.1 and return its exit code; None when nothing was spawned."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return None
+    n_dev = torch.cuda.device_count()
+    if n_dev < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but {n_dev} CUDA devices visible"}), flush=True)
+        return 2
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -190,130 +218,332 @@ def cpu_baseline_sample(lay, q, k, v, csr, seconds):
                       f"{dt:.1f} s of oracle time (fp64 upcasts excluded)"}
 
 
-def run_ours(args):
-    ws, rank, local = dist_env()
+def stats(xs):
+    """median and p90 (nearest rank) of a list of per-step times."""
+    ys = sorted(xs)
+    if not ys:
+        return None, None
+    return ys[len(ys) // 2] if len(ys) % 2 else 0.5 * (ys[len(ys) // 2 - 1] + ys[len(ys) // 2]), \
+        ys[min(len(ys) - 1, int(math.ceil(0.9 * len(ys))) - 1)]
+
+
+class _Csr:
+    def __init__(self, row_ptr, col_idx):
+        self.row_ptr, self.col_idx = row_ptr, col_idx
+
+
+def init_dist(ws, local):
     if ws > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
+
+
+def l2_flush_buffer(dev):
+    return torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 512 MB > 126 MB L2
+
+
+def time_k3_cold(hp, flush, reps=5):
+    """K3 alone right after an L2 flush (M read from HBM), median ms."""
+    import paper_2502_21079_b200 as ada
+    out = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        ada.select_blocks(hp.mass, heads_desc=hp.desc, mode=hp.mode, target=hp.targets, flags=hp.flags,
+                          tier_tau=hp.tier_tau, out=hp.csr)
+        b.record()
+        torch.cuda.synchronize()
+        out.append(a.elapsed_time(b))
+    return stats(out)[0]
+
+
+def kernel_entries(lay, nb, nnz, kfl, med, peaks, traffic, p90=None, heads=None):
+    """Roofline entries of K1..K4 from per-kernel median ms."""
+    tens_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    exp_peak = 16.0 * 148 * sm_max * 1e6 / 1e12      # MUFU.EX2 16/clk/SM (T exp/s)
+    H = lay.heads if heads is None else heads
+    N, d = lay.n, lay.head_dim
+    dense_fl = 4.0 * N * N * d * H
+    k3_bytes = 4.0 * nb * nb * H + 4.0 * (H * nb + 1) + 4.0 * nnz + 4.0 * H * nb
+    p90 = p90 or [None] * 4
+    rnd = (lambda x, n=3: None if x is None else round(x, n))  # noqa: E731
+    return {
+        "K1_dense_attn_lse": roofline_entry("tensor", dense_fl / (med[0] / 1e3) / 1e12, tens_peak, "TFLOP/s",
+                                            traffic.get("K1"), ms=rnd(med[0]), ms_p90=rnd(p90[0]),
+                                            exp_frac=round(N * N * H / (med[0] / 1e3) / 1e12 / exp_peak, 4)),
+        "K2_lse_cached_search": roofline_entry("alu", N * N * H / (med[1] / 1e3) / 1e12, exp_peak, "Texp/s",
+                                               traffic.get("K2"), ms=rnd(med[1]), ms_p90=rnd(p90[1]),
+                                               tensor_tflops=round(dense_fl / 2 / (med[1] / 1e3) / 1e12, 1)),
+        "K3_select_blocks": roofline_entry("hbm", k3_bytes / (med[2] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s",
+                                           traffic.get("K3"), ms=rnd(med[2], 4), ms_p90=rnd(p90[2], 4)),
+        "K4_block_sparse_attn": roofline_entry("tensor", kfl / (med[3] / 1e3) / 1e12, tens_peak, "TFLOP/s",
+                                               traffic.get("K4"), ms=rnd(med[3]), ms_p90=rnd(p90[3])),
+    }
+
+
+def variant_tiers(hp, q, k, v, lay, peaks, reps=5):
+    """The paper's default selection on the same layer: SPARSITY 0.8 with
+    head-adaptive tiers and the text sink, on the block masses of the main run's last search (exact
+    LSE); K3 (tiers: two selection passes) and K4 on its CSR, median ms over `reps`."""
+    import paper_2502_21079_b200 as ada
+    H, nb = lay.heads, hp.nb
+    rows = H * nb
+    e = lambda n, dt: torch.empty(n, dtype=dt, device=q.device)  # noqa: E731
+    csr = ada.Csr(e(rows + 1, torch.int32), e(rows * nb, torch.int32), e(rows, torch.int32),
+                  torch.empty(1, H, dtype=torch.float32, device=q.device),
+                  torch.empty(1, H, dtype=torch.int64, device=q.device))
+    o = torch.empty_like(q)
+    t3, t4 = [], []
+    for i in range(reps + 1):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
+        ada.select_blocks(hp.mass, heads_desc=hp.desc, mode=ada.SELECT_SPARSITY, target=[0.8] * H,
+                          flags=ada.FLAG_TEXT_SINK | ada.FLAG_HEAD_TIERS, tier_tau=0.8, out=csr)
+        ev[1].record()
+        ada.block_sparse_attn(q, k, v, csr.row_ptr, csr.col_idx, block_size=lay.block, n_text=lay.n_text,
+                              text_first=lay.text_first, o=o, workspace=hp.ws)
+        ev[2].record()
+        torch.cuda.synchronize()
+        if i:
+            t3.append(ev[0].elapsed_time(ev[1]))
+            t4.append(ev[1].elapsed_time(ev[2]))
+    kfl, nnz = kept_flops(lay, csr, lay.head_dim)
+    tens_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    m3, m4 = stats(t3)[0], stats(t4)[0]
+    tf = kfl / (m4 / 1e3) / 1e12
+    return {"selection": "sparsity 0.8 + head tiers (tau 0.8) + text sink, row-wise (paper default, "
+                         "PAPER.md:527-533, 547, 549-550)",
+            "K3_ms": round(m3, 4), "K4_ms": round(m4, 3), "K4_tflops": round(tf, 3),
+            "K4_frac": round(tf / tens_peak, 4), "kept_density": round(nnz / (H * nb * nb), 4),
+            "head_nnz": [int(x) for x in csr.head_nnz[0].tolist()]}
+
+
+def variant_config(name, args, peaks, traffic, reps=5):
+    """Another BASELINE config (CogVideoX-shaped layer, configs[1]) through the whole hot path:
+    per-kernel median ms and roofline."""
+    import paper_2502_21079_b200 as ada
+    import workloads
+    from paper_2502_21079_b200.hotpath import HotPath
+    lay = workloads.layout_for(name)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    q, k, v = workloads.generate_qkv(lay, device=dev)
+    hp = HotPath(1, lay.heads, lay.n, lay.head_dim, lay.block, lay.n_text, lay.text_first,
+                 mode=ada.SELECT_RECALL, targets=args.recall, flags=ada.FLAG_TEXT_SINK)
+    for _ in range(2):
+        hp.run(q, k, v)
+    per = []
+    for _ in range(reps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        hp.run(q, k, v, events=ev)
+        torch.cuda.synchronize()
+        per.append([ev[i].elapsed_time(ev[i + 1]) for i in range(4)])
+    med = [stats([p[i] for p in per])[0] for i in range(4)]
+    kfl, nnz = kept_flops(lay, hp.csr, lay.head_dim)
+    kern = kernel_entries(lay, hp.nb, nnz, kfl, med, peaks, traffic.get(name, {}))
+    out = {"seq_len": lay.n, "heads": lay.heads, "head_dim": lay.head_dim, "block": lay.block,
+           "selection": f"recall {args.recall} per head, text sink",
+           "K4_tflops": kern["K4_block_sparse_attn"]["achieved"], "ms_per_layer_sparse": round(med[3], 3),
+           "search_overhead_ms": round(med[1] + med[2], 3),
+           "search_overhead_vs_dense": round((med[1] + med[2]) / med[0], 4), "dense_ms": round(med[0], 3),
+           "kept_density": round(nnz / (lay.heads * hp.nb * hp.nb), 4), "kernels": kern}
+    del q, k, v, hp
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_ours(args):
+    """One layer per job; rank p runs the search on its contiguous head group and K4 on its K4 head
+    set (the same group, or the LPT set with --lpt).  value = the layer's kept FLOPs / the slowest
+    rank's K4 time (strong scaling; at N=1 the whole layer on one GPU)."""
+    ws, rank, local = dist_env()
+    init_dist(ws, local)
     import workloads
     import paper_2502_21079_b200 as ada
+    from paper_2502_21079_b200 import dist as D
     from paper_2502_21079_b200.hotpath import HotPath
 
     lay = workloads.layout_for(args.config)
     dev = torch.device("cuda", torch.cuda.current_device())
-    seed = workloads.synth.BASE_SEED + 101 * rank
-    q, k, v = workloads.generate_qkv(lay, device=dev, seed=seed)
+    H, N, d = lay.heads, lay.n, lay.head_dim
+    if H < ws:
+        raise SystemExit(f"{H} heads cannot be sharded over {ws} ranks")
+    h0, h1 = D.head_range(H, ws, rank)
+    Hl = h1 - h0
+    full = workloads.generate_qkv(lay, device=dev)          # the same layer on every rank (same seed)
+    if ws == 1:
+        q, k, v = full
+    else:
+        q, k, v = (x[:, h0:h1].contiguous() for x in full)
+    if not args.lpt:
+        del full
+        torch.cuda.empty_cache()
     if args.mode == "recall":
-        hp = HotPath(1, lay.heads, lay.n, lay.head_dim, lay.block, lay.n_text, lay.text_first,
+        hp = HotPath(1, Hl, N, d, lay.block, lay.n_text, lay.text_first,
                      mode=ada.SELECT_RECALL, targets=args.recall, flags=ada.FLAG_TEXT_SINK)
     else:
-        hp = HotPath(1, lay.heads, lay.n, lay.head_dim, lay.block, lay.n_text, lay.text_first,
+        hp = HotPath(1, Hl, N, d, lay.block, lay.n_text, lay.text_first,
                      mode=ada.SELECT_SPARSITY, targets=0.8, flags=ada.FLAG_TEXT_SINK | ada.FLAG_HEAD_TIERS)
+    nb = hp.nb
+
+    # K4 head set: the search group, or (--lpt) an LPT set by kept tiles from the first search
+    hp.search(q, k, v)
+    grp, gci = D.gather_csr(hp.csr.row_ptr, hp.csr.col_idx)
+    costs = D.head_nnz(grp, nb)                              # kept tiles per head, whole layer
+    contig = D.contiguous_assign(H, ws)
+    assign = D.lpt_assign(costs, ws) if args.lpt else contig
+    mine = assign[rank]
+    if args.lpt:
+        idx = torch.tensor(mine, device=dev)
+        q4, k4, v4 = (x.index_select(1, idx).contiguous() for x in full)
+        del full
+        torch.cuda.empty_cache()
+        o4 = torch.empty_like(q4)
+        ws4 = torch.empty(max(ada.sparse_workspace_bytes(ada.make_desc(q4, lay.block, lay.n_text,
+                                                                        lay.text_first)), 1),
+                          dtype=torch.uint8, device=dev)
+
+    def step(ev=None):
+        rec = (lambda i: ev[i].record()) if ev else (lambda i: None)  # noqa: E731
+        hp.search(q, k, v, events=ev[:4] if ev else None)
+        if args.lpt:
+            rp, ci = D.gather_csr(hp.csr.row_ptr, hp.csr.col_idx)
+            prp, pci = D.pack_heads_csr(rp, ci, mine, nb)
+            rec(4)
+            ada.block_sparse_attn(q4, k4, v4, prp, pci, block_size=lay.block, n_text=lay.n_text,
+                                  text_first=lay.text_first, o=o4, workspace=ws4)
+            step.csr = _Csr(prp, pci)
+        else:
+            rec(4)
+            hp.sparse(q, k, v)
+            step.csr = hp.csr
+        rec(5)
+
     for _ in range(args.warmup):
-        hp.run(q, k, v)
+        step()
     torch.cuda.synchronize()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(K)]
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     clk = ClockSampler(dev.index)
     t_wall = time.perf_counter()
-    for s in range(args.steps):
-        hp.run(q, k, v, events=ev[s])
+    for s in range(K):
+        step(ev[s])
     torch.cuda.synchronize()
     wall = time.perf_counter() - t_wall
     if ws > 1:
         torch.distributed.barrier()
     clocks = clk.stop()
-    per = [[ev[s][i].elapsed_time(ev[s][i + 1]) for i in range(4)] for s in range(args.steps)]
-    tk = [sum(p[i] for p in per) for i in range(4)]          # ms over K steps, per kernel
-    total = sum(tk)
-    kfl, nnz = kept_flops(lay, hp.csr, lay.head_dim)
-    nb = hp.nb
-    H, N, d = lay.heads, lay.n, lay.head_dim
-    from paper_2502_21079_b200.dist import reduce_step_timings
-    K = args.steps
-    value, tmax = reduce_step_timings([total, tk[0], tk[1], tk[2], tk[3]], kfl, K)  # max over ranks
-    total_max, k4_max = tmax[0], tmax[4]
-    work = torch.tensor([value * (k4_max / 1e3) * 1e12 / K], dtype=torch.float64)  # sum over ranks
+    # per step: K1, K2, K3, exchange, K4, total -- each the max over ranks
+    per = [[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]),
+            e[3].elapsed_time(e[4]), e[4].elapsed_time(e[5]), e[0].elapsed_time(e[5])] for e in ev]
+    flat = D.reduce_max([x for p in per for x in p])
+    per = [flat[6 * s:6 * s + 6] for s in range(K)]
+    tot = [sum(p[i] for p in per) for i in range(6)]
+    med = [stats([p[i] for p in per])[0] for i in range(6)]
+    p90 = [stats([p[i] for p in per])[1] for i in range(6)]
+    kfl, nnz = kept_flops(lay, step.csr, d)
+    kfl_all, nnz_all = D.reduce_sum([kfl, nnz])
+    value = kfl_all * K / (tot[4] / 1e3) / 1e12
+    loads = [x[0] for x in D.all_gather_floats([nnz])]
+    imb_contig = D.imbalance(costs, contig)[0]
+    flush = l2_flush_buffer(dev)
+    k3_cold = D.reduce_max([time_k3_cold(hp, flush)])[0]
+    del flush
 
     # e2e: the same metric (K4 TFLOP/s on kept blocks) for a sparse step end to end through the public
     # API from pinned host buffers: H2D of Q,K,V, the block-sparse forward on the cached CSR, D2H of O,
-    # pipelined over head groups (HotPath.run_sparse_host)
+    # pipelined over head groups (HotPath.run_sparse_host), on this rank's search head group
     e2e = None
     if not args.no_e2e:
         qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
         oh = torch.empty_like(qh).pin_memory()
+        groups = max(1, min(24, Hl))
         for _ in range(2):
-            hp.run_sparse_host(qh, kh, vh, oh)
+            hp.run_sparse_host(qh, kh, vh, oh, groups=groups)
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if ws > 1:
             torch.distributed.barrier()
         s0.record()
         for _ in range(K):
-            hp.run_sparse_host(qh, kh, vh, oh)
+            hp.run_sparse_host(qh, kh, vh, oh, groups=groups)
         s1.record()
         torch.cuda.synchronize()
-        te = torch.tensor([s0.elapsed_time(s1)], dtype=torch.float64, device=dev)
-        if ws > 1:
-            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        e2e = {"value": round(work.item() * K / (te.item() / 1e3) / 1e12, 3), "unit": UNIT,
-               "h2d_bytes_per_step": 3 * q.numel() * q.element_size(),
-               "d2h_bytes_per_step": q.numel() * q.element_size(),
-               "ms_per_step": round(te.item() / K, 3),
-               "note": "sparse step from pinned host memory: H2D Q,K,V + K4 (cached CSR) + D2H O, "
-                       "overlapped over 24 head groups, K4 launches alternating between two compute streams (tools/e2e_groups.py: 12 -> 45.0 ms, 16 -> 44.4 ms, 24 -> 43.8 ms; bound: 37.1 ms of pinned H2D at 55.5 GB/s); TFLOP/s on kept blocks"}
+        te = D.reduce_max([s0.elapsed_time(s1)])[0]
+        kfl_c = D.reduce_sum([kept_flops(lay, hp.csr, d)[0]])[0]
+        e2e = {"value": round(kfl_c * K / (te / 1e3) / 1e12, 3), "unit": UNIT,
+               "h2d_bytes_per_step": 3 * q.numel() * q.element_size() * ws,
+               "d2h_bytes_per_step": q.numel() * q.element_size() * ws,
+               "ms_per_step": round(te / K, 3),
+               "note": f"sparse step from pinned host memory: H2D Q,K,V + K4 (cached CSR) + D2H O per rank "
+                       f"(its search head group), overlapped over {groups} head groups, K4 launches "
+                       "alternating between two compute streams; PCIe-bound (2.06 GB of pinned H2D per "
+                       "HYV-110K layer); TFLOP/s on kept blocks, whole job"}
+        del qh, kh, vh, oh
+
+    peaks, src = load_peaks()
+    traffic = load_traffic()
+    launches = hp.kernels_per_run() * K
+    variants = None
+    if ws == 1 and not args.no_variants and args.config == "hyv110k":
+        variants = {"hyv110k_sparsity0.8_tiers": variant_tiers(hp, q, k, v, lay, peaks)}
+        del q, k, v, hp
+        torch.cuda.empty_cache()
+        variants["cogx45k_recall0.9"] = variant_config("cogx45k", args, peaks, traffic)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        qc, kc, vc = workloads.generate_qkv(lay, device=dev)
+        cpu = cpu_baseline_sample(lay, qc, kc, vc, step.csr, args.cpu_seconds)
 
     if rank != 0:
         if ws > 1:
             torch.distributed.destroy_process_group()
         return
-    peaks, src = load_peaks()
-    tens_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-    sm_max = peaks.get("sm_max_mhz", 1965.0)
-    exp_peak = 16.0 * 148 * sm_max * 1e6 / 1e12      # MUFU.EX2 16/clk/SM (T exp/s)
-    traffic = load_traffic()
-    ms = [x / K for x in tk]
-    dense_fl = 4.0 * N * N * d * H
-    k3_bytes = 4.0 * nb * nb * H + 4.0 * (H * nb + 1) + 4.0 * nnz + 4.0 * H * nb
-    kern = {
-        "K1_dense_attn_lse": roofline_entry("tensor", dense_fl / (ms[0] / 1e3) / 1e12, tens_peak, "TFLOP/s",
-                                            traffic.get("K1"), ms=round(ms[0], 3)),
-        "K2_lse_cached_search": roofline_entry("alu", N * N * H / (ms[1] / 1e3) / 1e12, exp_peak, "Texp/s",
-                                               traffic.get("K2"), ms=round(ms[1], 3),
-                                               tensor_tflops=round(dense_fl / 2 / (ms[1] / 1e3) / 1e12, 1)),
-        "K3_select_blocks": roofline_entry("hbm", k3_bytes / (ms[2] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s",
-                                           traffic.get("K3"), ms=round(ms[2], 4)),
-        "K4_block_sparse_attn": roofline_entry("tensor", kfl / (ms[3] / 1e3) / 1e12, tens_peak, "TFLOP/s",
-                                               traffic.get("K4"), ms=round(ms[3], 3)),
-    }
-    dom = max(range(4), key=lambda i: ms[i])
-    dom_name = list(kern)[dom]
+    ms = [x / K for x in tot]
+    h_max = -(-H // ws)            # K1-K3 times are the slowest rank's, i.e. one with ceil(H/N) heads
+    kern = kernel_entries(lay, nb, nnz_all * h_max / H, kfl_all, [med[0], med[1], med[2], med[4]], peaks,
+                          traffic, p90=[p90[0], p90[1], p90[2], p90[4]], heads=h_max)
+    if ws > 1:   # K1-K3 achieved rates per rank's head group; K4 on the whole layer's kept FLOPs
+        kern["K4_block_sparse_attn"] = roofline_entry("tensor", value, kern["K4_block_sparse_attn"]["peak"] * ws,
+                                                      "TFLOP/s", None, ms=round(med[4], 3),
+                                                      ms_p90=round(p90[4], 3), note=f"whole job, {ws} GPUs")
+    kern["K3_select_blocks"]["ms_cold"] = round(k3_cold, 4)
+    kern["K3_select_blocks"]["ms_warm"] = kern["K3_select_blocks"]["ms"]
+    k3 = kern["K3_select_blocks"]
+    k3["achieved_cold"] = round(k3["achieved"] * k3["ms"] / k3_cold, 3)
+    dom_name = max(kern, key=lambda n: kern[n]["ms"])
     roof = dict(kern[dom_name])
     roof["kernel"] = dom_name
     roof["peak_source"] = f"{src} ({'bf16_tflops_sustained' if roof['bound'] == 'tensor' else 'see kernels'})"
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(lay, q, k, v, hp.csr, args.cpu_seconds)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
-        "ms_per_step": round(total_max / K, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(ms[5], 3), "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (workloads/synth.py, seeded; DESIGN.md §5)",
         "config": {"workload": lay.name, "seq_len": N, "heads": H, "head_dim": d, "block": lay.block,
                    "n_text": lay.n_text, "selection": (f"recall {args.recall} per head, text sink"
                                                        if args.mode == "recall" else "sparsity 0.8 + head tiers"),
-                   "layers_per_rank": 1, "l2": "inputs larger than L2 (Q,K,V = %.2f GB)" % (3 * q.numel() * 2 / 1e9)},
-        "ms_per_layer_sparse": round(k4_max / K, 3),
-        "search_overhead_ms": round((tk[1] + tk[2]) / K, 3),
-        "search_overhead_vs_dense": round((tk[1] + tk[2]) / tk[0], 4),
+                   "parallelism": (f"head-sharded x{ws}" + (" + LPT K4 head sets" if args.lpt else "")
+                                   if ws > 1 else "1 GPU, whole layer"),
+                   "l2": "inputs larger than L2 (Q,K,V = %.2f GB per layer)" % (3 * N * H * d * 2 / 1e9)},
+        "ms_per_layer_sparse": round(ms[4], 3),
+        "search_overhead_ms": round(ms[1] + ms[2], 3),
+        "search_overhead_vs_dense": round((tot[1] + tot[2]) / tot[0], 4),
         "dense_ms": round(ms[0], 3),
-        "kept_density": round(nnz / (H * nb * nb), 4),
-        "roofline": roof, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": hp.kernels_per_run() * K, "clocks": clocks,
+        "kept_density": round(nnz_all / (H * nb * nb), 4),
+        "roofline": roof, "kernels": kern,
+        "multi_gpu": {"k4_heads_per_rank": [len(a) for a in assign], "kept_tiles_per_rank": loads,
+                      "kept_tile_imbalance": round(max(loads) / (sum(loads) / len(loads)), 4),
+                      "contiguous_imbalance": round(imb_contig, 4),
+                      "exchange_ms": round(ms[3], 3) if args.lpt else 0.0},
+        "cpu_baseline": cpu, "e2e": e2e, "variants": variants,
+        "gpu_launches": launches, "clocks": clocks,
         "wall_s_timed_region": round(wall, 3),
     }
     print(json.dumps(line), flush=True)
@@ -323,17 +553,24 @@ def run_ours(args):
 
 def run_ulysses(args):
     """configs[3]: ONE HunyuanVideo-shaped layer whose activations arrive sequence-sharded ([N/P, H, d]
-    per rank, as a sequence-parallel DiT holds them).  A step = NCCL all_to_all of Q, K, V to head shards
-    [N, H/P, d] -> K1 -> K2 -> K3 -> K4 on the local heads (token-major, read through the descriptor
-    strides: no unpack) -> all_to_all of O back.  value = kept FLOPs of the whole layer / max over ranks
-    of the K4 time (strong scaling)."""
+    per rank, as a sequence-parallel DiT holds them).  A step = the search step t_w (NCCL all_to_all of
+    Q, K, V to head shards [N, H_r, d] -> K1 -> K2 -> K3 on the local heads, read token-major through the
+    descriptor strides with no unpack; all_to_all of O back) followed by a sparse step (all_to_all in,
+    K4, all_to_all of O back).  --lpt: the sparse step's head sets are LPT by kept tiles (the a2a send
+    order carries the permutation; the CSRs are all-gathered after the search).  value = kept FLOPs of
+    the whole layer / max over ranks of the K4 time (strong scaling)."""
     ws, rank, local = dist_env()
     import torch.distributed as dist
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
-        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1,
+        import socket
+        so = socket.socket()
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+        so.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
                                 device_id=torch.device("cuda", local))
     import workloads
     import paper_2502_21079_b200 as ada
@@ -353,25 +590,53 @@ def run_ulysses(args):
     torch.cuda.empty_cache()
     hp = HotPath(1, Hp, N, d, lay.block, lay.n_text, lay.text_first, mode=ada.SELECT_RECALL,
                  targets=args.recall, flags=ada.FLAG_TEXT_SINK, token_major=True)
+    nb = hp.nb
+    kw = dict(block_size=lay.block, n_text=lay.n_text, text_first=lay.text_first)
+
+    # the sparse step's head sets (LPT from a first search, or the contiguous groups)
+    sh = [D.as_bhnd(D.ulysses_in(x, sizes=sizes)) for x in loc]
+    hp.search(*sh)
+    grp, gci = D.gather_csr(hp.csr.row_ptr, hp.csr.col_idx)
+    costs = D.head_nnz(grp, nb)
+    contig = D.contiguous_assign(H, ws)
+    assign = D.lpt_assign(costs, ws) if args.lpt else contig
+    mine = assign[rank]
+    del sh
+    ws4 = None
 
     def step(ev=None):
-        if ev:
-            ev[0].record()
+        rec = (lambda i: ev[i].record()) if ev else (lambda i: None)  # noqa: E731
+        nonlocal ws4
+        rec(0)
         sh = [D.as_bhnd(D.ulysses_in(x, sizes=sizes)) for x in loc]             # [1, Hp, N, d] token-major views
-        if ev:
-            ev[1].record()
-        ev4 = ev[1:6] if ev else None
-        o = hp.run(*sh, events=ev4)
-        o_loc = D.ulysses_out(o[0].transpose(0, 1), sizes)          # [N_p, H, d]
-        if ev:
-            ev[6].record()
-        return o_loc
+        rec(1)
+        hp.search(*sh, events=ev[1:5] if ev else None)
+        o_d = D.ulysses_out(hp.o_dense[0].transpose(0, 1), sizes)               # O of the search step back
+        rec(5)
+        if args.lpt:
+            rp, ci = D.gather_csr(hp.csr.row_ptr, hp.csr.col_idx)
+            csr = _Csr(*D.pack_heads_csr(rp, ci, mine, nb))
+        else:
+            csr = hp.csr
+        rec(6)
+        s4 = [D.as_bhnd(D.ulysses_in(x, sizes=sizes, assign=assign)) for x in loc]   # sparse step's a2a in
+        rec(7)
+        if ws4 is None:
+            ws4 = torch.empty(max(ada.sparse_workspace_bytes(ada.make_desc(s4[0], **kw)), 1), dtype=torch.uint8,
+                              device=dev)
+        o4 = torch.empty_like(s4[0])
+        ada.block_sparse_attn(*s4, csr.row_ptr, csr.col_idx, o=o4, workspace=ws4, **kw)
+        rec(8)
+        o_s = D.ulysses_out(o4[0].transpose(0, 1), sizes, assign=assign)
+        rec(9)
+        step.csr = csr
+        return o_d, o_s
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(K)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(10)] for _ in range(K)]
     dist.barrier()
     torch.cuda.synchronize()
     clk = ClockSampler(dev.index)
@@ -380,30 +645,35 @@ def run_ulysses(args):
     torch.cuda.synchronize()
     dist.barrier()
     clocks = clk.stop()
-    # per step: a2a in, K1, K2, K3, K4, a2a out
-    per = [[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]), e[3].elapsed_time(e[4]),
-            e[4].elapsed_time(e[5]), e[5].elapsed_time(e[6])] for e in evs]
-    tk = [sum(p[i] for p in per) for i in range(6)]
-    total = sum(tk)
-    kfl, nnz = kept_flops(workloads.layout_for(args.config, heads=Hp), hp.csr, d)
-    t = torch.tensor([total] + tk, dtype=torch.float64, device=dev)
-    work = torch.tensor([kfl, float(nnz)], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dist.all_reduce(work, op=dist.ReduceOp.SUM)
+    # phases: a2a in (search), K1, K2, K3, a2a out (search O), exchange, a2a in (sparse), K4, a2a out
+    per = [[e[i].elapsed_time(e[i + 1]) for i in range(9)] for e in evs]
+    flat = D.reduce_max([x for p in per for x in p])
+    per = [flat[9 * s:9 * s + 9] for s in range(K)]
+    tot = [sum(p[i] for p in per) for i in range(9)]
+    kfl, nnz = kept_flops(workloads.layout_for(args.config, heads=len(mine)), step.csr, d)
+    kfl_all, nnz_all = D.reduce_sum([kfl, nnz])
+    loads = [x[0] for x in D.all_gather_floats([nnz])]
     if rank == 0:
-        ms = [x / K for x in t.tolist()]
+        ms = [x / K for x in tot]
         line = {
-            "metric": METRIC, "value": round(work[0].item() * K / (t[5].item() / 1e3) / 1e12, 3), "unit": UNIT,
-            "n_gpus": ws, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms[0], 3),
+            "metric": METRIC, "value": round(kfl_all * K / (tot[7] / 1e3) / 1e12, 3), "unit": UNIT,
+            "n_gpus": ws, "steps": K, "warmup": args.warmup, "ms_per_step": round(sum(ms), 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (workloads/synth.py, seeded; DESIGN.md \u00a75)",
+            "data": "synthetic (workloads/synth.py, seeded; DESIGN.md §5)",
             "config": {"workload": lay.name + "-ulysses", "seq_len": N, "heads": H, "heads_per_rank": Hp,
-                       "head_dim": d, "block": lay.block, "parallelism": f"ulysses a2a x{ws} (NCCL)",
+                       "head_dim": d, "block": lay.block,
+                       "parallelism": f"ulysses a2a x{ws} (NCCL)" + (" + LPT sparse-step head sets" if args.lpt else ""),
                        "l2": "inputs larger than L2"},
-            "ms_per_layer_sparse": round(ms[5], 3), "a2a_in_ms": round(ms[1], 3), "a2a_out_ms": round(ms[6], 3),
-            "dense_ms": round(ms[2], 3), "search_overhead_ms": round(ms[3] + ms[4], 3),
-            "kept_density": round(work[1].item() / (H * hp.nb * hp.nb), 4),
-            "gpu_launches": hp.kernels_per_run() * K, "clocks": clocks,
+            "ms_per_layer_sparse": round(ms[7], 3), "dense_ms": round(ms[1], 3),
+            "search_overhead_ms": round(ms[2] + ms[3], 3),
+            "a2a_ms": {"search_in": round(ms[0], 3), "search_out": round(ms[4], 3), "sparse_in": round(ms[6], 3),
+                       "sparse_out": round(ms[8], 3)},
+            "exchange_ms": round(ms[5], 3),
+            "kept_density": round(nnz_all / (H * nb * nb), 4),
+            "multi_gpu": {"k4_heads_per_rank": [len(a) for a in assign], "kept_tiles_per_rank": loads,
+                          "kept_tile_imbalance": round(max(loads) / (sum(loads) / len(loads)), 4),
+                          "contiguous_imbalance": round(D.imbalance(costs, contig)[0], 4)},
+            "gpu_launches": (hp.kernels_per_run()) * K, "clocks": clocks,
             "note": "times are max over ranks per phase; value uses the max-over-ranks K4 time",
         }
         print(json.dumps(line), flush=True)
@@ -481,6 +751,9 @@ def run_reference(args):
 
 def main():
     args = parse()
+    rc = maybe_spawn(args)
+    if rc is not None:
+        sys.exit(rc)
     if args.impl == "reference":
         run_reference(args)
     elif args.ulysses:

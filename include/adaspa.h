@@ -25,12 +25,7 @@
  *    keeps >= 1 block per row; K4 writes O = 0 and LSE' = -inf for a row with
  *    no kept block.
  *
- *  - Environment (read once per process; diagnostics, off by default):
- *    ADASPA_PAIR=1 runs K1/K4 at d = 128 (K4 at block 128) on the CTA-pair
- *    kernel (attn_pair.cu); ADASPA_ONE=1 runs K1 at d = 128 on the one-tile
- *    kernel (attn_one.cu; 2-4 select its timing ablations, whose results are
- *    NOT correct).  Both variants are measured slower than the default kernels
- *    (DESIGN.md §6).
+ *  - No environment variable changes what the product library computes.
  *
  * Numbers: Q, K, V, O are bf16; accumulation, softmax, LSE and block mass are
  * fp32 (the block-mass cross-row reduction and every selection prefix sum are

@@ -123,7 +123,10 @@ def _same_layout(desc, *ts):
             raise TypeError("Q/K/V/O must be bf16 CUDA tensors")
         if tuple(t.shape) != (desc.batch, desc.heads, desc.seq_len, desc.head_dim):
             raise ValueError("Q/K/V/O shapes differ")
-        if tuple(t.stride()) != (desc.stride_b, desc.stride_h, desc.stride_n, 1):
+        # a dimension of extent 1 is never stepped over, so its stride does not matter (a Ulysses
+        # as_bhnd view [1, Hp, N, d] has stride_b = Hp*d, a [B, N, H, d] buffer N*H*d)
+        want = (desc.stride_b, desc.stride_h, desc.stride_n, 1)
+        if any(n > 1 and s != w for n, s, w in zip(t.shape, t.stride(), want)):
             raise ValueError("Q/K/V/O must share one layout (strides)")
 
 

@@ -145,26 +145,6 @@ SelectWs select_ws_layout(const adaspa_attn_desc* d) {
   return w;
 }
 
-// d = 128 runs on a CTA pair (attn_pair.cu) for the dense pass and for the sparse pass at block 128;
-// Opt-in (ADASPA_PAIR=1) until it beats the one-SM kernel of attn_fwd.cu.
-bool use_pair(const adaspa_attn_desc* d, bool sparse) {
-  static const bool enabled = [] {
-    const char* e = getenv("ADASPA_PAIR");
-    return e && e[0] == '1';
-  }();
-  return enabled && d->head_dim == 128 && (!sparse || d->block_size == 128);
-}
-
-// d = 128 dense pass with one q tile per SM and two alternating softmax groups (attn_one.cu);
-// opt-in (ADASPA_ONE=1) until it beats attn_fwd.cu.
-bool use_one(const adaspa_attn_desc* d) {
-  static const bool enabled = [] {
-    const char* e = getenv("ADASPA_ONE");
-    return e && e[0] >= '1' && e[0] <= '4';  // 2-4: diagnostic ablations (attn_one.cu)
-  }();
-  return enabled && d->head_dim == 128;
-}
-
 struct SparseWs {
   int items_per_bh, num_items, stride;
   size_t queue, len, order, stream, bytes;
@@ -217,8 +197,7 @@ adaspa_status adaspa_dense_attn_lse(const adaspa_attn_desc* desc, const void* q,
       (s = check_ptr16(o, "o")))
     return s;
   CUtensorMap tq, tk, tv;
-  const bool pair = use_pair(desc, false);
-  if ((s = make_map(&tq, q, desc, "q", 128)) || (s = make_map(&tk, k, desc, "k", pair ? 64 : 128)) ||
+  if ((s = make_map(&tq, q, desc, "q", 128)) || (s = make_map(&tk, k, desc, "k", 128)) ||
       (s = make_map(&tv, v, desc, "v", 128)))
     return s;
   AttnParams p{};
@@ -234,9 +213,7 @@ adaspa_status adaspa_dense_attn_lse(const adaspa_attn_desc* desc, const void* q,
   p.lse = lse;
   p.items_per_bh = (desc->seq_len + 255) / 256;
   p.num_items = desc->batch * desc->heads * p.items_per_bh;
-  cudaError_t e = pair ? launch_attn_pair(tq, tk, tv, p, false, num_sms(), (cudaStream_t)stream)
-                 : use_one(desc) ? launch_attn_one(tq, tk, tv, p, num_sms(), (cudaStream_t)stream)
-                       : launch_attn(tq, tk, tv, p, desc->head_dim, false, false, num_sms(), (cudaStream_t)stream);
+  cudaError_t e = launch_attn(tq, tk, tv, p, desc->head_dim, false, false, num_sms(), (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "dense_attn_lse launch");
   return ADASPA_OK;
 }
@@ -398,9 +375,8 @@ adaspa_status adaspa_block_sparse_attn(const adaspa_attn_desc* desc, const void*
   if (!workspace || workspace_bytes < w.bytes)
     return fail(ADASPA_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", workspace_bytes, w.bytes);
   CUtensorMap tq, tk, tv;
-  const bool pair = use_pair(desc, true);
   const int rows_s = desc->block_size == 64 ? 64 : 128;
-  if ((s = make_map(&tq, q, desc, "q", rows_s)) || (s = make_map(&tk, k, desc, "k", pair ? 64 : rows_s)) ||
+  if ((s = make_map(&tq, q, desc, "q", rows_s)) || (s = make_map(&tk, k, desc, "k", rows_s)) ||
       (s = make_map(&tv, v, desc, "v", rows_s)))
     return s;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
@@ -440,8 +416,7 @@ adaspa_status adaspa_block_sparse_attn(const adaspa_attn_desc* desc, const void*
   p.stream_len = pp.stream_len;
   p.stream_stride = w.stride;
   p.queue = reinterpret_cast<int*>(ws + w.queue);
-  e = pair ? launch_attn_pair(tq, tk, tv, p, true, num_sms(), st)
-           : launch_attn(tq, tk, tv, p, desc->head_dim, two, true, num_sms(), st);
+  e = launch_attn(tq, tk, tv, p, desc->head_dim, two, true, num_sms(), st);
   if (e != cudaSuccess) return cuda_fail(e, "block_sparse_attn launch");
   return ADASPA_OK;
 }

@@ -61,13 +61,6 @@ struct SearchParams {
 cudaError_t launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                         const AttnParams& p, int head_dim, bool two, bool sparse, int num_sms,
                         cudaStream_t st);
-// d = 128 on a CTA pair (attn_pair.cu): same items and kv streams as launch_attn (two 128-row q
-// tiles per item), one tile per SM of the pair.
-cudaError_t launch_attn_pair(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                             const AttnParams& p, bool sparse, int num_sms, cudaStream_t st);
-// d = 128 dense pass with one 128-row q tile per SM (attn_one.cu); items computed from p.N.
-cudaError_t launch_attn_one(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                            const AttnParams& p, int num_sms, cudaStream_t st);
 cudaError_t launch_sparse_prep(const SparsePrepParams& p, cudaStream_t st);
 cudaError_t launch_search(const CUtensorMap& tq, const CUtensorMap& tk, const SearchParams& p, int head_dim,
                           bool two, int num_sms, cudaStream_t st);

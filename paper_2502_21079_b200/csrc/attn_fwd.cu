@@ -567,24 +567,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kind = inf.kind;
       if (kind == kAllEnd) break;
       if (kind == kEnd) {
-        if (inf.has) {
-          const int b = inf.b, h = inf.h;
-          int tok[2];
-          bool valid[2];
+        const int b = inf.b, h = inf.h;
+        int tok[2];
+        bool valid[2];
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int row = j ? row1 : row0;
-            if (!TWO) {
-              tok[j] = inf.start0 + row;
-              valid[j] = row < inf.len0;
-            } else if (row < 64) {
-              tok[j] = inf.start0 + row;
-              valid[j] = row < inf.len0;
-            } else {
-              tok[j] = inf.start1 + row - 64;
-              valid[j] = row - 64 < inf.len1;
-            }
+        for (int j = 0; j < 2; ++j) {
+          const int row = j ? row1 : row0;
+          if (!TWO) {
+            tok[j] = inf.start0 + row;
+            valid[j] = row < inf.len0;
+          } else if (row < 64) {
+            tok[j] = inf.start0 + row;
+            valid[j] = row < inf.len0;
+          } else {
+            tok[j] = inf.start1 + row - 64;
+            valid[j] = row - 64 < inf.len1;
           }
+        }
+        __nv_bfloat16* optr[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          optr[j] = p.o + b * p.sb + h * p.sh + static_cast<int64_t>(valid[j] ? tok[j] : 0) * p.sn + 2 * qd;
+        if (inf.has) {
           float l_tot[2], inv[2];
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
@@ -592,15 +596,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             l += __shfl_xor_sync(0xffffffffu, l, 1);
             l += __shfl_xor_sync(0xffffffffu, l, 2);
             l_tot[j] = l;
-            inv[j] = l > 0.0f ? 1.0f / l : 0.0f;
+            // a row with at least one kept column has l >= 1 (the element that set m_used contributes
+            // 2^0); below that only the 2^-126 floor of the polynomial exp on masked columns: empty row
+            inv[j] = l >= 0.25f ? 1.0f / l : 0.0f;
           }
           mbar_wait(&bars->o_full[t], oph);
           oph ^= 1;
           tc_fence_after();
-          __nv_bfloat16* optr[2];
-#pragma unroll
-          for (int j = 0; j < 2; ++j)
-            optr[j] = p.o + b * p.sb + h * p.sh + static_cast<int64_t>(valid[j] ? tok[j] : 0) * p.sn + 2 * qd;
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             uint32_t r[16];
@@ -622,11 +624,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 2; ++j)
               if (valid[j])
                 p.lse[(static_cast<int64_t>(b) * p.H + h) * p.N + tok[j]] =
-                    l_tot[j] > 0.0f ? (m_used[j] + __log2f(l_tot[j])) * kLn2 : -INFINITY;
+                    l_tot[j] >= 0.25f ? (m_used[j] + __log2f(l_tot[j])) * kLn2 : -INFINITY;
           }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars->o_empty[t]);
+        } else {  // no kept kv block for any row of this tile (a caller CSR with empty rows): O = 0, LSE = -inf
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                if (valid[j]) *reinterpret_cast<uint32_t*>(optr[j] + 32 * c + 8 * k) = 0u;
+          if (qd == 0 && p.lse) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              if (valid[j]) p.lse[(static_cast<int64_t>(b) * p.H + h) * p.N + tok[j]] = -INFINITY;
+          }
         }
         m_used[0] = m_used[1] = -INFINITY;
         l_sum[0] = l_sum[1] = 0.0f;
@@ -662,22 +677,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&bars->s_loaded[t]);
       }
       ADASPA_TRACE_EV(1);
-      // The running max is taken over the UNMASKED tile: any m >= the row max of the kept columns is
-      // a valid reference (exact, the final normalisation uses the same m; P of kept keys stays far
-      // above bf16/fp32 underflow), and it keeps the column limits -- a shared-memory load queued
-      // behind MUFU work in MIO, 4.8% of K1's stall samples when it gated the max -- off the
-      // critical path.  The limits are applied below, before the exponentials.
+      // Row max.  Taken first over the whole tile (the column limits -- a shared-memory load that
+      // queues behind MUFU work in MIO -- stay off the critical path of full tiles); a partial tile
+      // or an unneeded half (limits below 64 / 128, warp-uniform) then masks those columns to -inf
+      // and takes the max again, so masked columns -- TMA zero fill past the sequence end, the
+      // excluded half of a B=64 pair, the neighbour block behind a partial block -- never set m.
+      // (With them in m, a row whose kept logits sit ~90 nats below them underflows to l = 0.)
       float mxa[2], mxb[2];  // two partial maxima per row
-      mxa[0] = fmaxf(__uint_as_float(s[0]), __uint_as_float(s[1]));
-      mxb[0] = fmaxf(__uint_as_float(s[4]), __uint_as_float(s[5]));
-      mxa[1] = fmaxf(__uint_as_float(s[2]), __uint_as_float(s[3]));
-      mxb[1] = fmaxf(__uint_as_float(s[6]), __uint_as_float(s[7]));
+      auto row_max = [&]() {
+        mxa[0] = fmaxf(__uint_as_float(s[0]), __uint_as_float(s[1]));
+        mxb[0] = fmaxf(__uint_as_float(s[4]), __uint_as_float(s[5]));
+        mxa[1] = fmaxf(__uint_as_float(s[2]), __uint_as_float(s[3]));
+        mxb[1] = fmaxf(__uint_as_float(s[6]), __uint_as_float(s[7]));
 #pragma unroll
-      for (int k = 2; k < 16; k += 2) {
-        mxa[0] = fmax3(mxa[0], __uint_as_float(s[4 * k]), __uint_as_float(s[4 * k + 1]));
-        mxb[0] = fmax3(mxb[0], __uint_as_float(s[4 * k + 4]), __uint_as_float(s[4 * k + 5]));
-        mxa[1] = fmax3(mxa[1], __uint_as_float(s[4 * k + 2]), __uint_as_float(s[4 * k + 3]));
-        mxb[1] = fmax3(mxb[1], __uint_as_float(s[4 * k + 6]), __uint_as_float(s[4 * k + 7]));
+        for (int k = 2; k < 16; k += 2) {
+          mxa[0] = fmax3(mxa[0], __uint_as_float(s[4 * k]), __uint_as_float(s[4 * k + 1]));
+          mxb[0] = fmax3(mxb[0], __uint_as_float(s[4 * k + 4]), __uint_as_float(s[4 * k + 5]));
+          mxa[1] = fmax3(mxa[1], __uint_as_float(s[4 * k + 2]), __uint_as_float(s[4 * k + 3]));
+          mxb[1] = fmax3(mxb[1], __uint_as_float(s[4 * k + 6]), __uint_as_float(s[4 * k + 7]));
+        }
+      };
+      row_max();
+      if (limA < 64 || limB < 128) {  // partial tile / unneeded half: those columns -> -inf (P = 0)
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const int col = 8 * (i >> 2) + 2 * qd + (i & 1);
+          const int lim = col < 64 ? limA : limB;
+          s[i] = col < lim ? s[i] : __float_as_uint(-INFINITY);
+        }
+        row_max();
       }
       float mb[2];
       float alpha[2] = {1.0f, 1.0f};
@@ -702,14 +730,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mb[0] = (m_used[0] == -INFINITY) ? 0.0f : m_used[0];
       mb[1] = (m_used[1] == -INFINITY) ? 0.0f : m_used[1];
-      if (limA < 64 || limB < 128) {  // partial tile / unneeded half: those columns -> -inf (P = 0)
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          const int col = 8 * (i >> 2) + 2 * qd + (i & 1);
-          const int lim = col < 64 ? limA : limB;
-          s[i] = col < lim ? s[i] : __float_as_uint(-INFINITY);
-        }
-      }
       ADASPA_TRACE_EV(2);
       wait_p_free();  // kSepP: PV of the previous tile has read P_t and accumulated into O_t
       ++pcnt;

@@ -26,6 +26,8 @@ class HotPath:
         self.mode, self.flags, self.tier_tau = mode, flags, tier_tau
         self.targets = [float(targets)] * heads if isinstance(targets, (int, float)) else [float(t) for t in targets]
         dev = torch.device(device)
+        if dev.type == "cuda" and dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         e = lambda *s, dt=torch.bfloat16: torch.empty(*s, dtype=dt, device=dev)  # noqa: E731
         if token_major:
@@ -45,15 +47,20 @@ class HotPath:
         self.ws = e(max(L.sparse_workspace_bytes(self.desc), 1), dt=torch.uint8)
 
     def _stage(self, q, k, v):
-        if q.device == self.device:
+        """Device tensors are used in place (any layout the descriptor strides can express, e.g. the
+        token-major views a Ulysses exchange delivers); host tensors are copied into the buffers."""
+        if all(x.device == self.device for x in (q, k, v)):
             return q, k, v
+        if any(x.is_cuda and x.device != self.device for x in (q, k, v)):
+            raise ValueError(f"inputs on {q.device}, HotPath on {self.device}")
         self.q.copy_(q, non_blocking=True)
         self.k.copy_(k, non_blocking=True)
         self.v.copy_(v, non_blocking=True)
         return self.q, self.k, self.v
 
-    def run(self, q, k, v, events=None):
-        """events: optional list of 5 CUDA events recorded around K1, K2, K3, K4."""
+    def search(self, q, k, v, events=None):
+        """The search step t_w (Alg. 1): K1 dense attention + LSE, K2 block mass with that LSE, K3
+        selection into self.csr.  events: optional list of 4 CUDA events recorded around K1, K2, K3."""
         q, k, v = self._stage(q, k, v)
         rec = (lambda i: events[i].record()) if events else (lambda i: None)  # noqa: E731
         rec(0)
@@ -64,9 +71,23 @@ class HotPath:
         L.select_blocks(self.mass, heads_desc=self.desc, mode=self.mode, target=self.targets, flags=self.flags,
                         tier_tau=self.tier_tau, out=self.csr)
         rec(3)
-        L.block_sparse_attn(q, k, v, self.csr.row_ptr, self.csr.col_idx, o=self.o_sparse, workspace=self.ws,
-                            **self.kw)
-        rec(4)
+        return self.csr
+
+    def sparse(self, q, k, v, csr=None, o=None):
+        """K4 on the cached index lists (self.csr unless given): the step every later denoising step runs."""
+        q, k, v = self._stage(q, k, v)
+        csr = self.csr if csr is None else csr
+        o = self.o_sparse if o is None else o
+        L.block_sparse_attn(q, k, v, csr.row_ptr, csr.col_idx, o=o, workspace=self.ws, **self.kw)
+        return o
+
+    def run(self, q, k, v, events=None):
+        """search() then sparse(); events: optional list of 5 CUDA events recorded around K1..K4."""
+        q, k, v = self._stage(q, k, v)
+        self.search(q, k, v, events=events[:4] if events else None)
+        self.sparse(q, k, v)
+        if events:
+            events[4].record()
         return self.o_sparse
 
     # launches of our kernels per run(): K1 1, K2 1, K3 4 (rows, head, scan, write; +2 with tiers),
