@@ -262,7 +262,8 @@ def time_k3_cold(hp, flush, reps=5):
 
 
 def kernel_entries(lay, nb, nnz, kfl, med, peaks, traffic, p90=None, heads=None):
-    """Roofline entries of K1..K4 from per-kernel median ms."""
+    """Roofline entries of the path's kernels from per-kernel median ms.  med / p90:
+    dicts with keys K1, FS (fused search, optional), K2, K3, K4."""
     tens_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     sm_max = peaks.get("sm_max_mhz", 1965.0)
     exp_peak = 16.0 * 148 * sm_max * 1e6 / 1e12      # MUFU.EX2 16/clk/SM (T exp/s)
@@ -270,20 +271,29 @@ def kernel_entries(lay, nb, nnz, kfl, med, peaks, traffic, p90=None, heads=None)
     N, d = lay.n, lay.head_dim
     dense_fl = 4.0 * N * N * d * H
     k3_bytes = 4.0 * nb * nb * H + 4.0 * (H * nb + 1) + 4.0 * nnz + 4.0 * H * nb
-    p90 = p90 or [None] * 4
+    p90 = p90 or {}
     rnd = (lambda x, n=3: None if x is None else round(x, n))  # noqa: E731
-    return {
-        "K1_dense_attn_lse": roofline_entry("tensor", dense_fl / (med[0] / 1e3) / 1e12, tens_peak, "TFLOP/s",
-                                            traffic.get("K1"), ms=rnd(med[0]), ms_p90=rnd(p90[0]),
-                                            exp_frac=round(N * N * H / (med[0] / 1e3) / 1e12 / exp_peak, 4)),
-        "K2_lse_cached_search": roofline_entry("alu", N * N * H / (med[1] / 1e3) / 1e12, exp_peak, "Texp/s",
-                                               traffic.get("K2"), ms=rnd(med[1]), ms_p90=rnd(p90[1]),
-                                               tensor_tflops=round(dense_fl / 2 / (med[1] / 1e3) / 1e12, 1)),
-        "K3_select_blocks": roofline_entry("hbm", k3_bytes / (med[2] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s",
-                                           traffic.get("K3"), ms=rnd(med[2], 4), ms_p90=rnd(p90[2], 4)),
-        "K4_block_sparse_attn": roofline_entry("tensor", kfl / (med[3] / 1e3) / 1e12, tens_peak, "TFLOP/s",
-                                               traffic.get("K4"), ms=rnd(med[3]), ms_p90=rnd(p90[3])),
+    out = {
+        "K1_dense_attn_lse": roofline_entry("tensor", dense_fl / (med["K1"] / 1e3) / 1e12, tens_peak, "TFLOP/s",
+                                            traffic.get("K1"), ms=rnd(med["K1"]), ms_p90=rnd(p90.get("K1")),
+                                            exp_frac=round(N * N * H / (med["K1"] / 1e3) / 1e12 / exp_peak, 4)),
     }
+    if med.get("FS"):
+        # algorithmic work of the fused search = the dense pass's 4N^2dH: the block masses reuse its
+        # exponentials (no second QK^T); plus the block-LSE bytes written and read (4*(nb+1)*N per head)
+        out["K1K2_fused_search"] = roofline_entry(
+            "tensor", dense_fl / (med["FS"] / 1e3) / 1e12, tens_peak, "TFLOP/s", traffic.get("FS"),
+            ms=rnd(med["FS"]), ms_p90=rnd(p90.get("FS")),
+            blse_gb=round(2 * 4.0 * (nb + 1) * N * H / 1e9, 3),
+            note="dense pass + block LSEs (attn_fwd_kernel kModeBlse) then block_mass_kernel, one C-ABI call")
+    out["K2_lse_cached_search"] = roofline_entry("alu", N * N * H / (med["K2"] / 1e3) / 1e12, exp_peak, "Texp/s",
+                                                 traffic.get("K2"), ms=rnd(med["K2"]), ms_p90=rnd(p90.get("K2")),
+                                                 tensor_tflops=round(dense_fl / 2 / (med["K2"] / 1e3) / 1e12, 1))
+    out["K3_select_blocks"] = roofline_entry("hbm", k3_bytes / (med["K3"] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s",
+                                             traffic.get("K3"), ms=rnd(med["K3"], 4), ms_p90=rnd(p90.get("K3"), 4))
+    out["K4_block_sparse_attn"] = roofline_entry("tensor", kfl / (med["K4"] / 1e3) / 1e12, tens_peak, "TFLOP/s",
+                                                 traffic.get("K4"), ms=rnd(med["K4"]), ms_p90=rnd(p90.get("K4")))
+    return out
 
 
 def variant_tiers(hp, q, k, v, lay, peaks, reps=5):
@@ -334,22 +344,39 @@ def variant_config(name, args, peaks, traffic, reps=5):
     q, k, v = workloads.generate_qkv(lay, device=dev)
     hp = HotPath(1, lay.heads, lay.n, lay.head_dim, lay.block, lay.n_text, lay.text_first,
                  mode=ada.SELECT_RECALL, targets=args.recall, flags=ada.FLAG_TEXT_SINK)
+    o_warm = torch.empty_like(q)
+
+    def one(ev=None):
+        rec = (lambda i: ev[i].record()) if ev else (lambda i: None)  # noqa: E731
+        rec(0)
+        hp.dense(q, k, v, o=o_warm)
+        hp.search(q, k, v, events=[ev[1], ev[2], ev[6], ev[3]] if ev else None, fused=True)
+        hp.sparse(q, k, v)
+        rec(4)
+        hp.cached_search(q, k)
+        rec(5)
+
     for _ in range(2):
-        hp.run(q, k, v)
+        one()
     per = []
     for _ in range(reps):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-        hp.run(q, k, v, events=ev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        one(ev)
         torch.cuda.synchronize()
-        per.append([ev[i].elapsed_time(ev[i + 1]) for i in range(4)])
-    med = [stats([p[i] for p in per])[0] for i in range(4)]
+        per.append({"K1": ev[0].elapsed_time(ev[1]), "FS": ev[1].elapsed_time(ev[2]), "K3": ev[6].elapsed_time(ev[3]),
+                    "K4": ev[3].elapsed_time(ev[4]), "K2": ev[4].elapsed_time(ev[5])})
+    med = {n: stats([p[n] for p in per])[0] for n in per[0]}
     kfl, nnz = kept_flops(lay, hp.csr, lay.head_dim)
     kern = kernel_entries(lay, hp.nb, nnz, kfl, med, peaks, traffic.get(name, {}))
     out = {"seq_len": lay.n, "heads": lay.heads, "head_dim": lay.head_dim, "block": lay.block,
            "selection": f"recall {args.recall} per head, text sink",
-           "K4_tflops": kern["K4_block_sparse_attn"]["achieved"], "ms_per_layer_sparse": round(med[3], 3),
-           "search_overhead_ms": round(med[1] + med[2], 3),
-           "search_overhead_vs_dense": round((med[1] + med[2]) / med[0], 4), "dense_ms": round(med[0], 3),
+           "K4_tflops": kern["K4_block_sparse_attn"]["achieved"], "ms_per_layer_sparse": round(med["K4"], 3),
+           "search_overhead_ms": round(med["FS"] - med["K1"] + med["K3"], 3),
+           "search_overhead_vs_dense": round((med["FS"] - med["K1"] + med["K3"]) / med["K1"], 4),
+           "search_overhead_cached_vs_dense": round((med["K2"] + med["K3"]) / med["K1"], 4),
+           "t_w_step_ms": {"fused": round(med["FS"] + med["K3"], 3),
+                           "two_pass_k1_k2_k3": round(med["K1"] + med["K2"] + med["K3"], 3)},
+           "dense_ms": round(med["K1"], 3),
            "kept_density": round(nnz / (lay.heads * hp.nb * hp.nb), 4), "kernels": kern}
     del q, k, v, hp
     torch.cuda.empty_cache()
@@ -407,9 +434,19 @@ def run_ours(args):
                                                                         lay.text_first)), 1),
                           dtype=torch.uint8, device=dev)
 
+    o_warm = torch.empty_like(q)
+    lse_warm = torch.empty(1, Hl, N, dtype=torch.float32, device=dev)
+
+    # One step exercises every row of the path, in schedule order:
+    #   K1 (a warm-up step: dense attention + LSE) | fused search at t_w (K1 + K2 with the fresh LSE in
+    #   one dense pass, then the block-mass reduction) | K3 | [--lpt: CSR exchange] | K4 (a sparse step
+    #   on the cached CSR) | K2 (a later key step: block masses with the cached t_w LSE, Alg. 2)
+    # events: 0 K1 1 fused 2 (2b) K3 3 exchange 4 K4 5 K2 6
     def step(ev=None):
         rec = (lambda i: ev[i].record()) if ev else (lambda i: None)  # noqa: E731
-        hp.search(q, k, v, events=ev[:4] if ev else None)
+        rec(0)
+        hp.dense(q, k, v, o=o_warm, lse=lse_warm)
+        hp.search(q, k, v, events=[ev[1], ev[2], ev[7], ev[3]] if ev else None, fused=True)
         if args.lpt:
             rp, ci = D.gather_csr(hp.csr.row_ptr, hp.csr.col_idx)
             prp, pci = D.pack_heads_csr(rp, ci, mine, nb)
@@ -422,12 +459,14 @@ def run_ours(args):
             hp.sparse(q, k, v)
             step.csr = hp.csr
         rec(5)
+        hp.cached_search(q, k)
+        rec(6)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(K)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(K)]
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -440,17 +479,19 @@ def run_ours(args):
     if ws > 1:
         torch.distributed.barrier()
     clocks = clk.stop()
-    # per step: K1, K2, K3, exchange, K4, total -- each the max over ranks
-    per = [[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]),
-            e[3].elapsed_time(e[4]), e[4].elapsed_time(e[5]), e[0].elapsed_time(e[5])] for e in ev]
+    # per step: K1, fused search, K3, exchange, K4, K2 (cached LSE), total -- each the max over ranks
+    NP = 7
+    per = [[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[7].elapsed_time(e[3]), e[3].elapsed_time(e[4]),
+            e[4].elapsed_time(e[5]), e[5].elapsed_time(e[6]), e[0].elapsed_time(e[6])] for e in ev]
     flat = D.reduce_max([x for p in per for x in p])
-    per = [flat[6 * s:6 * s + 6] for s in range(K)]
-    tot = [sum(p[i] for p in per) for i in range(6)]
-    med = [stats([p[i] for p in per])[0] for i in range(6)]
-    p90 = [stats([p[i] for p in per])[1] for i in range(6)]
+    per = [flat[NP * s:NP * s + NP] for s in range(K)]
+    tot = [sum(p[i] for p in per) for i in range(NP)]
+    med = [stats([p[i] for p in per])[0] for i in range(NP)]
+    p90 = [stats([p[i] for p in per])[1] for i in range(NP)]
+    I_K1, I_FS, I_K3, I_X, I_K4, I_K2, I_TOT = range(NP)
     kfl, nnz = kept_flops(lay, step.csr, d)
     kfl_all, nnz_all = D.reduce_sum([kfl, nnz])
-    value = kfl_all * K / (tot[4] / 1e3) / 1e12
+    value = kfl_all * K / (tot[I_K4] / 1e3) / 1e12
     loads = [x[0] for x in D.all_gather_floats([nnz])]
     imb_contig = D.imbalance(costs, contig)[0]
     flush = l2_flush_buffer(dev)
@@ -490,7 +531,7 @@ def run_ours(args):
 
     peaks, src = load_peaks()
     traffic = load_traffic()
-    launches = hp.kernels_per_run() * K
+    launches = (hp.kernels_per_run() + 2) * K   # + K1 alone and K2 (cached LSE) per step
     variants = None
     if ws == 1 and not args.no_variants and args.config == "hyv110k":
         variants = {"hyv110k_sparsity0.8_tiers": variant_tiers(hp, q, k, v, lay, peaks)}
@@ -508,12 +549,13 @@ def run_ours(args):
         return
     ms = [x / K for x in tot]
     h_max = -(-H // ws)            # K1-K3 times are the slowest rank's, i.e. one with ceil(H/N) heads
-    kern = kernel_entries(lay, nb, nnz_all * h_max / H, kfl_all, [med[0], med[1], med[2], med[4]], peaks,
-                          traffic, p90=[p90[0], p90[1], p90[2], p90[4]], heads=h_max)
+    keys = {"K1": I_K1, "FS": I_FS, "K2": I_K2, "K3": I_K3, "K4": I_K4}
+    kern = kernel_entries(lay, nb, nnz_all * h_max / H, kfl_all, {n: med[i] for n, i in keys.items()}, peaks,
+                          traffic, p90={n: p90[i] for n, i in keys.items()}, heads=h_max)
     if ws > 1:   # K1-K3 achieved rates per rank's head group; K4 on the whole layer's kept FLOPs
         kern["K4_block_sparse_attn"] = roofline_entry("tensor", value, kern["K4_block_sparse_attn"]["peak"] * ws,
-                                                      "TFLOP/s", None, ms=round(med[4], 3),
-                                                      ms_p90=round(p90[4], 3), note=f"whole job, {ws} GPUs")
+                                                      "TFLOP/s", None, ms=round(med[I_K4], 3),
+                                                      ms_p90=round(p90[I_K4], 3), note=f"whole job, {ws} GPUs")
     kern["K3_select_blocks"]["ms_cold"] = round(k3_cold, 4)
     kern["K3_select_blocks"]["ms_warm"] = kern["K3_select_blocks"]["ms"]
     k3 = kern["K3_select_blocks"]
@@ -524,7 +566,7 @@ def run_ours(args):
     roof["peak_source"] = f"{src} ({'bf16_tflops_sustained' if roof['bound'] == 'tensor' else 'see kernels'})"
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
-        "ms_per_step": round(ms[5], 3), "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
+        "ms_per_step": round(ms[I_TOT], 3), "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (workloads/synth.py, seeded; DESIGN.md §5)",
         "config": {"workload": lay.name, "seq_len": N, "heads": H, "head_dim": d, "block": lay.block,
                    "n_text": lay.n_text, "selection": (f"recall {args.recall} per head, text sink"
@@ -532,16 +574,22 @@ def run_ours(args):
                    "parallelism": (f"head-sharded x{ws}" + (" + LPT K4 head sets" if args.lpt else "")
                                    if ws > 1 else "1 GPU, whole layer"),
                    "l2": "inputs larger than L2 (Q,K,V = %.2f GB per layer)" % (3 * N * H * d * 2 / 1e9)},
-        "ms_per_layer_sparse": round(ms[4], 3),
-        "search_overhead_ms": round(ms[1] + ms[2], 3),
-        "search_overhead_vs_dense": round((tot[1] + tot[2]) / tot[0], 4),
-        "dense_ms": round(ms[0], 3),
+        "ms_per_layer_sparse": round(ms[I_K4], 3),
+        # search overhead at t_w: what the fused search adds to a dense pass, plus K3
+        "search_overhead_ms": round(ms[I_FS] - ms[I_K1] + ms[I_K3], 3),
+        "search_overhead_vs_dense": round((tot[I_FS] - tot[I_K1] + tot[I_K3]) / tot[I_K1], 4),
+        # at a later key step (Alg. 2: no dense pass runs; K2 with the cached LSE, then K3)
+        "search_overhead_cached_ms": round(ms[I_K2] + ms[I_K3], 3),
+        "search_overhead_cached_vs_dense": round((tot[I_K2] + tot[I_K3]) / tot[I_K1], 4),
+        "t_w_step_ms": {"fused": round(ms[I_FS] + ms[I_K3], 3),
+                        "two_pass_k1_k2_k3": round(ms[I_K1] + ms[I_K2] + ms[I_K3], 3)},
+        "dense_ms": round(ms[I_K1], 3),
         "kept_density": round(nnz_all / (H * nb * nb), 4),
         "roofline": roof, "kernels": kern,
         "multi_gpu": {"k4_heads_per_rank": [len(a) for a in assign], "kept_tiles_per_rank": loads,
                       "kept_tile_imbalance": round(max(loads) / (sum(loads) / len(loads)), 4),
                       "contiguous_imbalance": round(imb_contig, 4),
-                      "exchange_ms": round(ms[3], 3) if args.lpt else 0.0},
+                      "exchange_ms": round(ms[I_X], 3) if args.lpt else 0.0},
         "cpu_baseline": cpu, "e2e": e2e, "variants": variants,
         "gpu_launches": launches, "clocks": clocks,
         "wall_s_timed_region": round(wall, 3),
@@ -664,8 +712,8 @@ def run_ulysses(args):
                        "head_dim": d, "block": lay.block,
                        "parallelism": f"ulysses a2a x{ws} (NCCL)" + (" + LPT sparse-step head sets" if args.lpt else ""),
                        "l2": "inputs larger than L2"},
-            "ms_per_layer_sparse": round(ms[7], 3), "dense_ms": round(ms[1], 3),
-            "search_overhead_ms": round(ms[2] + ms[3], 3),
+            "ms_per_layer_sparse": round(ms[7], 3), "t_w_fused_search_ms": round(ms[1], 3),
+            "k3_ms": round(ms[3], 3),
             "a2a_ms": {"search_in": round(ms[0], 3), "search_out": round(ms[4], 3), "sparse_in": round(ms[6], 3),
                        "sparse_out": round(ms[8], 3)},
             "exchange_ms": round(ms[5], 3),

@@ -9,6 +9,11 @@
  *   adaspa_select_blocks      K3  head-adaptive hierarchical selection -> CSR
  *   adaspa_block_sparse_attn  K4  block-sparse attention forward on the CSR
  *
+ * plus the fused search step t_w, K1 and K2 with the
+ * fresh LSE in one dense pass:
+ *
+ *   adaspa_dense_attn_lse_search  K1+K2  dense forward + LSE + block mass
+ *
  * Conventions (all functions):
  *  - Plain pointers only.  Every tensor argument is a DEVICE pointer owned by
  *    the caller unless its comment says "host".  The library allocates no
@@ -111,6 +116,33 @@ int32_t adaspa_num_blocks(const adaspa_attn_desc* desc);
  */
 adaspa_status adaspa_dense_attn_lse(const adaspa_attn_desc* desc, const void* q, const void* k,
                                     const void* v, void* o, float* lse, adaspa_stream_t stream);
+
+/*
+ * K1+K2 fused -- the search step t_w (Alg. 1 whole; W_sum_attn,
+ * PAPER.md:428-434, reading R4), with the outputs of K1 followed by K2 on the
+ * fresh LSE:
+ *   o, lse      as adaspa_dense_attn_lse (lse may be NULL),
+ *   block_mass  fp32 [B,H,nb,nb]: sum_{i in p} sum_{t in j} exp(scale*q_i.k_t - lse_i).
+ * Algorithm: ONE dense pass over the kv blocks of the grid; besides O and the
+ * row LSE it writes every per-(row, kv block) log-sum-exp
+ *   log2 sum_{t in j} 2^(scale*log2e*q_i.k_t)  (relative to a per-row reference)
+ * to the workspace, from the exponentials the pass computes anyway; a second,
+ * HBM-bound kernel forms block_mass = sum_i 2^(blockLSE_ij - LSE_i).  Exact up
+ * to rounding (no second QK^T, no second pass of exponentials over S).  Alg. 2
+ * (later key steps, cached LSE) stays adaspa_lse_cached_search.
+ * workspace: device scratch of >= adaspa_fused_search_workspace_bytes(desc, 1)
+ * bytes (4*(nb+1)*N bytes per head and batch element: 0.39 GB per head at
+ * HunyuanVideo-110K); heads are processed in passes of as many heads as fit
+ * (a workspace of adaspa_fused_search_workspace_bytes(desc, 0) runs all heads
+ * in one pass).  Too small: ADASPA_ERR_WORKSPACE_TOO_SMALL, nothing launched.
+ */
+adaspa_status adaspa_dense_attn_lse_search(const adaspa_attn_desc* desc, const void* q, const void* k,
+                                           const void* v, void* o, float* lse, float* block_mass,
+                                           void* workspace, size_t workspace_bytes, adaspa_stream_t stream);
+
+/* Workspace bytes of adaspa_dense_attn_lse_search for passes of `heads_per_pass`
+ * heads (<= 0 or > H: all heads in one pass). */
+size_t adaspa_fused_search_workspace_bytes(const adaspa_attn_desc* desc, int32_t heads_per_pass);
 
 /*
  * K2 -- LSE-cached online search (Alg. 2; Alg. 1 second

@@ -50,6 +50,8 @@ SYMBOLS = {
     "adaspa_num_blocks": (ctypes.c_int32, [_D]),
     "adaspa_dense_attn_lse": (ctypes.c_int, [_D, _P, _P, _P, _P, _P, _P]),
     "adaspa_lse_cached_search": (ctypes.c_int, [_D, _P, _P, _P, _P, _P]),
+    "adaspa_dense_attn_lse_search": (ctypes.c_int, [_D, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "adaspa_fused_search_workspace_bytes": (ctypes.c_size_t, [_D, ctypes.c_int32]),
     "adaspa_select_workspace_bytes": (ctypes.c_size_t, [_D]),
     "adaspa_select_blocks": (ctypes.c_int, [_D, _P, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_uint32,
                                              ctypes.c_double, _P, _P, ctypes.c_int64, _P, _P, _P, _P,
@@ -149,6 +151,36 @@ def dense_attn_lse(q, k, v, *, block_size, n_text, text_first=False, softmax_sca
     _check(_lib.adaspa_dense_attn_lse(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
                                       _stream(stream)), "adaspa_dense_attn_lse")
     return o, lse
+
+
+def fused_search_workspace_bytes(desc, heads_per_pass=0):
+    return int(_lib.adaspa_fused_search_workspace_bytes(ctypes.byref(desc), int(heads_per_pass)))
+
+
+def dense_attn_lse_search(q, k, v, *, block_size, n_text, text_first=False, softmax_scale=0.0, o=None, lse=None,
+                          block_mass=None, workspace=None, heads_per_pass=0, stream=None):
+    """K1 + K2 fused (the search step t_w, Alg. 1 in one dense pass): O, the row LSE and the block
+    masses with that LSE.  workspace: a uint8 CUDA tensor (allocated for `heads_per_pass` heads if
+    None; 0 = all heads in one pass).  Returns (o, lse, block_mass)."""
+    desc = make_desc(q, block_size, n_text, text_first, softmax_scale)
+    if o is None:
+        o = torch.empty_like(q)
+    _same_layout(desc, q, k, v, o)
+    nb = num_blocks(desc)
+    if lse is None:
+        lse = torch.empty(desc.batch, desc.heads, desc.seq_len, dtype=torch.float32, device=q.device)
+    _check_f32(lse, (desc.batch, desc.heads, desc.seq_len), "lse")
+    if block_mass is None:
+        block_mass = torch.empty(desc.batch, desc.heads, nb, nb, dtype=torch.float32, device=q.device)
+    _check_f32(block_mass, (desc.batch, desc.heads, nb, nb), "block_mass")
+    if workspace is None:
+        workspace = _scratch(fused_search_workspace_bytes(desc, heads_per_pass), q.device, stream)
+    if workspace.dtype != torch.uint8 or not workspace.is_cuda:
+        raise ValueError("workspace must be a uint8 CUDA tensor")
+    _check(_lib.adaspa_dense_attn_lse_search(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
+                                             _ptr(block_mass), _ptr(workspace), workspace.numel(),
+                                             _stream(stream)), "adaspa_dense_attn_lse_search")
+    return o, lse, block_mass
 
 
 def lse_cached_search(q, k, lse, *, block_size, n_text, text_first=False, softmax_scale=0.0, block_mass=None,

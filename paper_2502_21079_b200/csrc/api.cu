@@ -123,6 +123,11 @@ adaspa_status make_map(CUtensorMap* map, const void* base, const adaspa_attn_des
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// fused search workspace per (batch element, head): block LSEs [nb][N] + row LSEs [N], fp32
+size_t fused_head_bytes(const adaspa_attn_desc* d) {
+  return sizeof(float) * (static_cast<size_t>(make_grid(d).nb) + 1) * static_cast<size_t>(d->seq_len);
+}
+
 struct SelectWs {
   size_t bits, nnz, kept, total, kbh, loff, hcnt, hbase, hist, bytes;
 };
@@ -211,10 +216,80 @@ adaspa_status adaspa_dense_attn_lse(const adaspa_attn_desc* desc, const void* q,
   p.sh = desc->stride_h;
   p.sn = desc->stride_n;
   p.lse = lse;
+  p.h0 = 0;
+  p.nh = desc->heads;
   p.items_per_bh = (desc->seq_len + 255) / 256;
   p.num_items = desc->batch * desc->heads * p.items_per_bh;
-  cudaError_t e = launch_attn(tq, tk, tv, p, desc->head_dim, false, false, num_sms(), (cudaStream_t)stream);
+  cudaError_t e = launch_attn(tq, tk, tv, p, desc->head_dim, false, kModeDense, num_sms(), (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "dense_attn_lse launch");
+  return ADASPA_OK;
+}
+
+size_t adaspa_fused_search_workspace_bytes(const adaspa_attn_desc* desc, int32_t heads_per_pass) {
+  if (check_desc(desc) != ADASPA_OK) return 0;
+  const int hp = (heads_per_pass <= 0 || heads_per_pass > desc->heads) ? desc->heads : heads_per_pass;
+  return fused_head_bytes(desc) * static_cast<size_t>(desc->batch) * hp;
+}
+
+adaspa_status adaspa_dense_attn_lse_search(const adaspa_attn_desc* desc, const void* q, const void* k, const void* v,
+                                           void* o, float* lse, float* block_mass, void* workspace,
+                                           size_t workspace_bytes, adaspa_stream_t stream) {
+  adaspa_status s;
+  if ((s = check_desc(desc)) != ADASPA_OK) return s;
+  if ((s = check_ptr16(q, "q")) || (s = check_ptr16(k, "k")) || (s = check_ptr16(v, "v")) ||
+      (s = check_ptr16(o, "o")))
+    return s;
+  if (!block_mass) return fail(ADASPA_ERR_INVALID_ARG, "block_mass must not be NULL");
+  if (reinterpret_cast<uintptr_t>(block_mass) % 4 || reinterpret_cast<uintptr_t>(lse) % 4)
+    return fail(ADASPA_ERR_INVALID_ARG, "lse / block_mass misaligned");
+  const size_t per_head = fused_head_bytes(desc) * static_cast<size_t>(desc->batch);
+  if (!workspace || workspace_bytes < per_head)
+    return fail(ADASPA_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes (one head of every batch element)",
+                workspace_bytes, per_head);
+  const int hc = static_cast<int>(workspace_bytes / per_head < (size_t)desc->heads ? workspace_bytes / per_head
+                                                                                   : (size_t)desc->heads);
+  CUtensorMap tq, tk, tv;
+  const int rows_kv = desc->block_size == 64 ? 64 : 128;
+  if ((s = make_map(&tq, q, desc, "q", 128)) || (s = make_map(&tk, k, desc, "k", rows_kv)) ||
+      (s = make_map(&tv, v, desc, "v", rows_kv)))
+    return s;
+  const BlockGrid g = make_grid(desc);
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int h0 = 0; h0 < desc->heads; h0 += hc) {
+    const int nh = desc->heads - h0 < hc ? desc->heads - h0 : hc;
+    float* blse = static_cast<float*>(workspace);
+    float* lrel = blse + static_cast<size_t>(desc->batch) * nh * g.nb * desc->seq_len;
+    AttnParams p{};
+    p.B = desc->batch;
+    p.H = desc->heads;
+    p.N = desc->seq_len;
+    p.grid = g;
+    p.scale_log2 = scale_of(desc) * kLog2e;
+    p.o = static_cast<__nv_bfloat16*>(o);
+    p.sb = desc->stride_b;
+    p.sh = desc->stride_h;
+    p.sn = desc->stride_n;
+    p.lse = lse;
+    p.h0 = h0;
+    p.nh = nh;
+    p.items_per_bh = (desc->seq_len + 255) / 256;
+    p.num_items = desc->batch * nh * p.items_per_bh;
+    p.blse = blse;
+    p.lrel = lrel;
+    cudaError_t e = launch_attn(tq, tk, tv, p, desc->head_dim, desc->block_size == 64, kModeBlse, num_sms(), st);
+    if (e != cudaSuccess) return cuda_fail(e, "dense_attn_lse_search launch (dense pass)");
+    BlockMassParams m{};
+    m.B = desc->batch;
+    m.H = desc->heads;
+    m.N = desc->seq_len;
+    m.h0 = h0;
+    m.nh = nh;
+    m.grid = g;
+    m.blse = blse;
+    m.lrel = lrel;
+    m.mass = block_mass;
+    if ((e = launch_block_mass(m, st)) != cudaSuccess) return cuda_fail(e, "dense_attn_lse_search launch (block mass)");
+  }
   return ADASPA_OK;
 }
 
@@ -409,6 +484,8 @@ adaspa_status adaspa_block_sparse_attn(const adaspa_attn_desc* desc, const void*
   p.sh = desc->stride_h;
   p.sn = desc->stride_n;
   p.lse = lse;
+  p.h0 = 0;
+  p.nh = desc->heads;
   p.items_per_bh = w.items_per_bh;
   p.num_items = w.num_items;
   p.item_order = pp.item_order;
@@ -416,7 +493,7 @@ adaspa_status adaspa_block_sparse_attn(const adaspa_attn_desc* desc, const void*
   p.stream_len = pp.stream_len;
   p.stream_stride = w.stride;
   p.queue = reinterpret_cast<int*>(ws + w.queue);
-  e = launch_attn(tq, tk, tv, p, desc->head_dim, two, true, num_sms(), st);
+  e = launch_attn(tq, tk, tv, p, desc->head_dim, two, kModeSparse, num_sms(), st);
   if (e != cudaSuccess) return cuda_fail(e, "block_sparse_attn launch");
   return ADASPA_OK;
 }

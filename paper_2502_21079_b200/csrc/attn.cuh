@@ -17,8 +17,11 @@ __host__ __device__ __forceinline__ int entry_id1(uint64_t e) { return static_ca
 __host__ __device__ __forceinline__ uint32_t entry_mask(uint64_t e) { return static_cast<uint32_t>(e >> 32); }
 constexpr int kMaxSparseBlocks = 65535;
 
+enum : int { kModeDense = 0, kModeBlse = 1, kModeSparse = 2 };
+
 struct AttnParams {
   int B, H, N;
+  int h0, nh;                // heads [h0, h0 + nh) of the H in the tensors (items cover B * nh heads)
   BlockGrid grid;
   float scale_log2;          // softmax_scale * log2(e)
   __nv_bfloat16* o;          // output, same strides as Q/K/V
@@ -32,6 +35,22 @@ struct AttnParams {
   const int* stream_len;     // [num_items]
   int stream_stride;
   int* queue;                // atomic work counter
+  // kModeBlse only (fused search at t_w): per (row, kv block) log-sum-exps and per-row LSEs, both in
+  // log2 units relative to the row's first running max ref_i (small magnitudes keep them exact):
+  //   blse[((b*nh + h-h0)*nb + kb)*N + i] = log2 sum_{j in kb} 2^(s_ij*scale*log2e) - ref_i
+  //   lrel[(b*nh + h-h0)*N + i]           = log2 sum_j     2^(s_ij*scale*log2e) - ref_i
+  float* blse;
+  float* lrel;
+};
+
+// Fused search, second half: block_mass[b,h,qb,kb] = sum_{i in qb} 2^(blse[.., kb, i] - lrel[.., i])
+struct BlockMassParams {
+  int B, H, N;
+  int h0, nh;
+  BlockGrid grid;
+  const float* blse;
+  const float* lrel;
+  float* mass;               // [B, H, nb, nb]
 };
 
 struct SparsePrepParams {
@@ -59,8 +78,9 @@ struct SearchParams {
 };
 
 cudaError_t launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                        const AttnParams& p, int head_dim, bool two, bool sparse, int num_sms,
+                        const AttnParams& p, int head_dim, bool two, int mode, int num_sms,
                         cudaStream_t st);
+cudaError_t launch_block_mass(const BlockMassParams& p, cudaStream_t st);
 cudaError_t launch_sparse_prep(const SparsePrepParams& p, cudaStream_t st);
 cudaError_t launch_search(const CUtensorMap& tq, const CUtensorMap& tk, const SearchParams& p, int head_dim,
                           bool two, int num_sms, cudaStream_t st);

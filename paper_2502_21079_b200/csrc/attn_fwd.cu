@@ -85,6 +85,7 @@ enum : int { kNormal = 0, kEnd = 1, kAllEnd = 2 };
 
 struct SlotMeta {
   int kind, mask, len0, len1;
+  int id0, id1;  // kv block ids of the entry's two 64-row halves (grid / sparse modes)
 };
 
 struct TileInfo {
@@ -93,6 +94,7 @@ struct TileInfo {
   int has;         // END: this tile had >= 1 entry in the item (O must be stored)
   int b, h;
   int start0, len0, start1, len1;
+  int kb0, kb1;    // BLSE mode, normal tiles: kv block ids of the tile (kb1 = -1: one block per tile)
 };
 
 struct ItemInfo {
@@ -127,8 +129,8 @@ struct Bars {
 __device__ __forceinline__ void decode_item(const AttnParams& p, bool sparse, bool two, int id, ItemInfo& it) {
   const int bh = id / p.items_per_bh;
   const int pi = id - bh * p.items_per_bh;
-  it.b = bh / p.H;
-  it.h = bh - it.b * p.H;
+  it.b = bh / p.nh;
+  it.h = p.h0 + (bh - it.b * p.nh);
   if (!sparse) {
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
@@ -169,10 +171,17 @@ __device__ __forceinline__ void decode_item(const AttnParams& p, bool sparse, bo
 static_assert(sizeof(Bars) <= 2048, "barrier block outgrew its reservation");
 static_assert(Smem<128>::kBytes <= 232448 && Smem<64>::kBytes <= 232448, "over 227 KB of shared memory");
 
-template <int D, bool TWO, bool SPARSE>
+// MODE: kDense (K1: 128-row kv tiles from token 0), kBlse (K1 + block LSEs: kv tiles follow the
+// block grid -- one block per tile, or two 64-row blocks with KVTWO -- and every (row, kv block)
+// log-sum-exp is written for the fused block-mass reduction), kSparse (K4: the merged CSR stream).
+// QTWO: a q tile is two 64-row q-blocks (sparse B=64); KVTWO: a kv tile is two 64-row kv blocks.
+template <int D, bool QTWO, bool KVTWO, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, const AttnParams p) {
+  constexpr bool SPARSE = MODE == kModeSparse;
+  constexpr bool GRID = MODE != kModeDense;  // kv tiles follow the block grid
+  constexpr bool BLSE = MODE == kModeBlse;
   using S = Smem<D>;
   constexpr int NS = S::kNS;
   constexpr bool kSepP = D == 64;
@@ -242,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (item >= p.num_items) break;
         const int id = SPARSE ? __ldg(p.item_order + item) : item;
         ItemInfo it;
-        decode_item(p, SPARSE, TWO, id, it);
+        decode_item(p, SPARSE, QTWO, id, it);
         mbar_wait(&bars->q_empty, qph ^ 1);
         qph ^= 1;
         bars->qitem = it;
@@ -250,32 +259,42 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive_expect_tx(&bars->q_full, qbytes);
         for (int t = 0; t < 2; ++t) {
           if (!it.exists[t]) continue;
-          const int r1 = TWO ? it.start1[t] : it.start0[t] + 64;
+          const int r1 = QTWO ? it.start1[t] : it.start0[t] + 64;
           for (int c = 0; c < CH; ++c) {
             uint8_t* dst = sQ + t * TILE + c * CHUNK;
             tma_load_4d_hint(&tq, &bars->q_full, dst, c * 64, it.start0[t], it.h, it.b, pol_q);
-            if (TWO) tma_load_4d_hint(&tq, &bars->q_full, dst + CHUNK / 2, c * 64, r1, it.h, it.b, pol_q);  // B=64: second block; else one 128-row box
+            if (QTWO) tma_load_4d_hint(&tq, &bars->q_full, dst + CHUNK / 2, c * 64, r1, it.h, it.b, pol_q);  // B=64: second block; else one 128-row box
           }
         }
-        const int n_ent = SPARSE ? __ldg(p.stream_len + id) : (p.N + 127) / 128;
+        const int n_ent = SPARSE ? __ldg(p.stream_len + id)
+                          : GRID ? (KVTWO ? (p.grid.nb + 1) / 2 : p.grid.nb) : (p.N + 127) / 128;
         const uint64_t* ent_ptr = SPARSE ? p.stream + static_cast<int64_t>(id) * p.stream_stride : nullptr;
         const uint32_t dense_mask = (it.exists[0] ? 0x0Fu : 0u) | (it.exists[1] ? 0xF0u : 0u);
         for (int e = 0; e < n_ent; ++e) {
-          int s0, l0, s1, l1;
+          int s0, l0, s1, l1, id0 = -1, id1 = -1;
           uint32_t mask;
           if (SPARSE) {
             const uint64_t ent = __ldg(reinterpret_cast<const unsigned long long*>(ent_ptr) + e);
-            const int id0 = entry_id0(ent), id1 = entry_id1(ent);
+            id0 = entry_id0(ent);
+            id1 = entry_id1(ent);
             mask = entry_mask(ent);
             s0 = p.grid.start(id0);
             l0 = p.grid.len(id0);
-            if (TWO) {
+            if (KVTWO) {
               s1 = p.grid.start(id1);
               l1 = p.grid.len(id1);
             } else {
               s1 = s0 + 64;
               l1 = 0;
             }
+          } else if (GRID) {  // every kv block of the head, in order (one per tile, or two 64-row blocks)
+            id0 = KVTWO ? 2 * e : e;
+            id1 = (KVTWO && id0 + 1 < p.grid.nb) ? id0 + 1 : -1;
+            s0 = p.grid.start(id0);
+            l0 = p.grid.len(id0);
+            s1 = id1 >= 0 ? p.grid.start(id1) : s0 + 64;
+            l1 = id1 >= 0 ? p.grid.len(id1) : 0;
+            mask = dense_mask;
           } else {
             s0 = 128 * e;
             l0 = p.N - s0 < 128 ? p.N - s0 : 128;
@@ -287,12 +306,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           ADASPA_TRACE_TMA(0);
           mbar_wait(&bars->kv_empty[slot], ph ^ 1);
           ADASPA_TRACE_TMA(1);
-          bars->meta[slot] = SlotMeta{kNormal, static_cast<int>(mask), l0, l1};
+          bars->meta[slot] = SlotMeta{kNormal, static_cast<int>(mask), l0, l1, id0, id1};
           mbar_arrive_expect_tx(&bars->kv_full[slot], TILE);
           for (int c = 0; c < CH; ++c) {
             uint8_t* dst = sKV + slot * TILE + c * CHUNK;
             tma_load_4d_hint(&tk, &bars->kv_full[slot], dst, c * 64, s0, it.h, it.b, pol_kv);
-            if (TWO) tma_load_4d_hint(&tk, &bars->kv_full[slot], dst + CHUNK / 2, c * 64, s1, it.h, it.b, pol_kv);  // B=64: second block; else one 128-row box
+            if (KVTWO) tma_load_4d_hint(&tk, &bars->kv_full[slot], dst + CHUNK / 2, c * 64, s1, it.h, it.b, pol_kv);  // B=64: second block; else one 128-row box
           }
           if (++slot == NS) { slot = 0; ph ^= 1; }
           // V
@@ -303,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < CH; ++c) {
             uint8_t* dst = sKV + slot * TILE + c * CHUNK;
             tma_load_4d_hint(&tv, &bars->kv_full[slot], dst, c * 64, s0, it.h, it.b, pol_kv);
-            if (TWO) tma_load_4d_hint(&tv, &bars->kv_full[slot], dst + CHUNK / 2, c * 64, s1, it.h, it.b, pol_kv);  // B=64: second block; else one 128-row box
+            if (KVTWO) tma_load_4d_hint(&tv, &bars->kv_full[slot], dst + CHUNK / 2, c * 64, s1, it.h, it.b, pol_kv);  // B=64: second block; else one 128-row box
           }
           if (++slot == NS) { slot = 0; ph ^= 1; }
         }
@@ -481,13 +500,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int hq = 0; hq < 2; ++hq) {
                 const uint32_t bits = (need >> (2 * hq)) & 3u;
-                if (!TWO) {
+                if (!KVTWO) {
                   inf.lim[hq * 2 + 0] = (bits & 1u) ? (mt.len0 < 64 ? mt.len0 : 64) : 0;
                   inf.lim[hq * 2 + 1] = (bits & 2u) ? mt.len0 : 64;
                 } else {
                   inf.lim[hq * 2 + 0] = (bits & 1u) ? mt.len0 : 0;
                   inf.lim[hq * 2 + 1] = (bits & 2u) ? 64 + mt.len1 : 64;
                 }
+              }
+              if (BLSE) {
+                inf.b = it.b;
+                inf.h = it.h;
+                inf.start0 = it.start0[t];
+                inf.len0 = it.len0[t];
+                inf.kb0 = mt.id0;
+                inf.kb1 = mt.id1;
               }
               tc_commit(&bars->s_full[t]);
               mbar_arrive(&bars->s_full[t]);
@@ -553,10 +580,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     int icnt = 0;
     float m_used[2] = {-INFINITY, -INFINITY};
     float l_sum[2] = {0.0f, 0.0f};  // this thread's share (its 32 columns) of the row sums
+    float ref[2] = {0.0f, 0.0f};    // BLSE: the row's first running max (log2 units)
     int ntile = 0;
     int tr_k = 0;
     (void)tr_k;
     const Poly3x2 poly;
+    // BLSE: the block sums feed the block masses, so the FMA-pipe exponentials use the degree-5
+    // polynomial (rel. error 2.3e-7, ex2.approx class) instead of the degree-3 one (7.5e-5, enough
+    // for P's bf16 rounding but not for a block mass to ~1e-6)
+    const Poly5x2 poly5;
     for (;;) {
       mbar_wait(&bars->s_full[t], sph);
       sph ^= 1;
@@ -573,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int row = j ? row1 : row0;
-          if (!TWO) {
+          if (!QTWO) {
             tok[j] = inf.start0 + row;
             valid[j] = row < inf.len0;
           } else if (row < 64) {
@@ -626,6 +658,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 p.lse[(static_cast<int64_t>(b) * p.H + h) * p.N + tok[j]] =
                     l_tot[j] >= 0.25f ? (m_used[j] + __log2f(l_tot[j])) * kLn2 : -INFINITY;
           }
+          if (BLSE && qd == 1) {  // the row LSE relative to ref (log2 units), for the block-mass reduction
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              if (valid[j])
+                p.lrel[(static_cast<int64_t>(b) * p.nh + (h - p.h0)) * p.N + tok[j]] =
+                    l_tot[j] >= 0.25f ? (m_used[j] - ref[j]) + __log2f(l_tot[j]) : -INFINITY;
+          }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars->o_empty[t]);
@@ -645,6 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         m_used[0] = m_used[1] = -INFINITY;
         l_sum[0] = l_sum[1] = 0.0f;
+        ref[0] = ref[1] = 0.0f;
         ntile = 0;
         continue;
       }
@@ -677,12 +717,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&bars->s_loaded[t]);
       }
       ADASPA_TRACE_EV(1);
-      // Row max.  Taken first over the whole tile (the column limits -- a shared-memory load that
-      // queues behind MUFU work in MIO -- stay off the critical path of full tiles); a partial tile
-      // or an unneeded half (limits below 64 / 128, warp-uniform) then masks those columns to -inf
-      // and takes the max again, so masked columns -- TMA zero fill past the sequence end, the
-      // excluded half of a B=64 pair, the neighbour block behind a partial block -- never set m.
-      // (With them in m, a row whose kept logits sit ~90 nats below them underflows to l = 0.)
+      // Row max over the whole tile first: the column limits (a shared-memory load that queues
+      // behind MUFU work in MIO) stay off the critical path of full tiles.  A partial tile or an
+      // unneeded half (limits below 64 / 128, warp-uniform; rare) then masks those columns to -inf
+      // and redoes the running-max update from the saved state with the max of the kept columns, so
+      // masked columns -- TMA zero fill past the sequence end, the excluded half of a B=64 pair, the
+      // neighbour block behind a partial block -- never set m.  (With them in m, a row whose kept
+      // logits sit ~90 nats below them would underflow to l = 0.)
       float mxa[2], mxb[2];  // two partial maxima per row
       auto row_max = [&]() {
         mxa[0] = fmaxf(__uint_as_float(s[0]), __uint_as_float(s[1]));
@@ -698,6 +739,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
       row_max();
+      float mb[2];
+      float alpha[2] = {1.0f, 1.0f};
+      bool rescale = false;
+      const float m_prev[2] = {m_used[0], m_used[1]};
+      const float l_prev[2] = {l_sum[0], l_sum[1]};
+      // m_used moves when the quad's row max exceeds it by more than 2^8 (log2 units)
+      auto update_max = [&](const float lmx0, const float lmx1) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          float mx = j ? lmx1 : lmx0;
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+          const float m_new = fmaxf(m_used[j], mx);
+          if (m_new > m_used[j] + kRescaleThreshold) {  // also true when m_used == -inf
+            alpha[j] = (m_used[j] == -INFINITY) ? 0.0f : exp2f(m_used[j] - m_new);
+            l_sum[j] *= alpha[j];
+            if (BLSE && m_used[j] == -INFINITY) ref[j] = m_new;
+            m_used[j] = m_new;
+            rescale |= alpha[j] != 0.0f && ntile > 0;
+          }
+        }
+      };
+      {
+        const float lmx0 = fmaxf(mxa[0], mxb[0]) * sl2, lmx1 = fmaxf(mxa[1], mxb[1]) * sl2;
+        // the quad's row max is needed only when some thread's max passes m_used + 8: one warp vote
+        // instead of four shuffles (which queue behind MUFU in MIO)
+        if (__any_sync(0xffffffffu, lmx0 > m_used[0] + kRescaleThreshold || lmx1 > m_used[1] + kRescaleThreshold))
+          update_max(lmx0, lmx1);
+      }
       if (limA < 64 || limB < 128) {  // partial tile / unneeded half: those columns -> -inf (P = 0)
 #pragma unroll
         for (int i = 0; i < 64; ++i) {
@@ -706,27 +776,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           s[i] = col < lim ? s[i] : __float_as_uint(-INFINITY);
         }
         row_max();
-      }
-      float mb[2];
-      float alpha[2] = {1.0f, 1.0f};
-      bool rescale = false;
-      float lmx[2] = {fmaxf(mxa[0], mxb[0]) * sl2, fmaxf(mxa[1], mxb[1]) * sl2};
-      // m_used only moves when the row max grows past it by more than 2^8, so the quad's row max is
-      // needed only then: one warp vote instead of four shuffles (which queue behind MUFU in MIO).
-      if (__any_sync(0xffffffffu, lmx[0] > m_used[0] + kRescaleThreshold || lmx[1] > m_used[1] + kRescaleThreshold)) {
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          float mx = lmx[j];
-          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-          const float m_new = fmaxf(m_used[j], mx);
-          if (m_new > m_used[j] + kRescaleThreshold) {  // also true when m_used == -inf
-            alpha[j] = (m_used[j] == -INFINITY) ? 0.0f : exp2f(m_used[j] - m_new);
-            l_sum[j] *= alpha[j];
-            m_used[j] = m_new;
-            rescale |= alpha[j] != 0.0f && ntile > 0;
-          }
-        }
+        m_used[0] = m_prev[0];
+        m_used[1] = m_prev[1];
+        l_sum[0] = l_prev[0];
+        l_sum[1] = l_prev[1];
+        alpha[0] = alpha[1] = 1.0f;
+        rescale = false;
+        update_max(fmaxf(mxa[0], mxb[0]) * sl2, fmaxf(mxa[1], mxb[1]) * sl2);
       }
       mb[0] = (m_used[0] == -INFINITY) ? 0.0f : m_used[0];
       mb[1] = (m_used[1] == -INFINITY) ? 0.0f : m_used[1];
@@ -751,6 +807,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float2 nm0 = make_float2(-mb[0], -mb[0]);
       const float2 nm1 = make_float2(-mb[1], -mb[1]);
       float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      float half0[2] = {0.0f, 0.0f};  // BLSE with KVTWO: the row sums of kv block id0 (columns 0-63)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t pk[16];
@@ -761,8 +818,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 x1 = ffma2(make_float2(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])), sl2v, nm1);
           float2 p0, p1;
           if (kExpPolyMod > 0 && (k % (kExpPolyMod > 0 ? kExpPolyMod : 1)) == kExpPolyMod - 1) {
-            p0 = exp2_poly3x2(x0, poly);
-            p1 = exp2_poly3x2(x1, poly);
+            if (BLSE) {
+              p0 = exp2_poly5x2(x0, poly5);
+              p1 = exp2_poly5x2(x1, poly5);
+            } else {
+              p0 = exp2_poly3x2(x0, poly);
+              p1 = exp2_poly3x2(x1, poly);
+            }
           } else {
             p0.x = ex2_approx(x0.x);
             p0.y = ex2_approx(x0.y);
@@ -780,16 +842,54 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars->p_half[t]);
+          if (BLSE && KVTWO) {  // kv block id0 ends here: keep its row sums apart from block id1's
+            const float2 h0 = fadd2(acc[0], acc[2]), h1 = fadd2(acc[1], acc[3]);
+            half0[0] = h0.x + h0.y;
+            half0[1] = h1.x + h1.y;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i] = make_float2(0.f, 0.f);
+          }
         }
       }
       const float2 a0 = fadd2(acc[0], acc[2]), a1 = fadd2(acc[1], acc[3]);
-      l_sum[0] += a0.x + a0.y;
-      l_sum[1] += a1.x + a1.y;
+      const float tsum[2] = {a0.x + a0.y, a1.x + a1.y};  // (KVTWO BLSE: kv block id1 only)
+      l_sum[0] += tsum[0] + half0[0];
+      l_sum[1] += tsum[1] + half0[1];
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       ADASPA_TRACE_EV(3);
       if (lane == 0) mbar_arrive(&bars->p_full[t]);
+      if (BLSE) {
+        // Off the critical path (P is handed over): the tile's per-(row, kv block) sums, quad-reduced,
+        // as log-sum-exps relative to the row's ref: log2 sum_{j in kb} 2^(s_ij*scale*log2e) - ref_i
+        // = log2(t) + (m_used - ref).  Quad lane qd writes (row qd&1, block half qd>>1), rows of a warp
+        // contiguous in blse[bh][kb][.] (16 rows x 4 B per store instruction and block).
+        // transpose-reduce over the quad: each exchange halves the values a lane keeps, so lane qd
+        // ends with value qd (row qd&1, half qd>>1) in 2 shuffles (one block) or 3 (KVTWO), not 4 / 8
+        const int j = qd & 1, hf = qd >> 1;
+        float tt;
+        if (KVTWO) {
+          // values: (r0,h0) (r1,h0) (r0,h1) (r1,h1); xor 2 splits the halves, xor 1 the rows
+          const float keep0 = hf ? tsum[0] : half0[0], send0 = hf ? half0[0] : tsum[0];
+          const float keep1 = hf ? tsum[1] : half0[1], send1 = hf ? half0[1] : tsum[1];
+          const float r0 = keep0 + __shfl_xor_sync(0xffffffffu, send0, 2);
+          const float r1 = keep1 + __shfl_xor_sync(0xffffffffu, send1, 2);
+          const float keep = j ? r1 : r0, send = j ? r0 : r1;
+          tt = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+        } else {
+          const float keep = j ? tsum[1] : tsum[0], send = j ? tsum[0] : tsum[1];
+          tt = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+          tt += __shfl_xor_sync(0xffffffffu, tt, 2);
+        }
+        const int kb = hf ? inf.kb1 : inf.kb0;
+        const int row = j ? row1 : row0;
+        if ((KVTWO || hf == 0) && kb >= 0 && row < inf.len0) {
+          const float Lb = tt > 0x1p-100f ? __log2f(tt) + (m_used[j] - ref[j]) : -INFINITY;
+          const int64_t bhl = static_cast<int64_t>(inf.b) * p.nh + (inf.h - p.h0);
+          p.blse[(bhl * p.grid.nb + kb) * p.N + inf.start0 + row] = Lb;
+        }
+      }
       ++ntile;
     }
   }
@@ -962,10 +1062,10 @@ cudaError_t launch_sparse_prep(const SparsePrepParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int D, bool TWO, bool SPARSE>
+template <int D, bool QTWO, bool KVTWO, int MODE>
 static cudaError_t launch_one(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                               const AttnParams& p, int num_sms, cudaStream_t st) {
-  auto kern = attn_fwd_kernel<D, TWO, SPARSE>;
+  auto kern = attn_fwd_kernel<D, QTWO, KVTWO, MODE>;
   const int smem = Smem<D>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -975,17 +1075,22 @@ static cudaError_t launch_one(const CUtensorMap& tq, const CUtensorMap& tk, cons
   return cudaGetLastError();
 }
 
+template <int D>
+static cudaError_t launch_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                            const AttnParams& p, bool two, int mode, int num_sms, cudaStream_t st) {
+  if (mode == kModeDense) return launch_one<D, false, false, kModeDense>(tq, tk, tv, p, num_sms, st);
+  if (mode == kModeBlse)
+    return two ? launch_one<D, false, true, kModeBlse>(tq, tk, tv, p, num_sms, st)
+               : launch_one<D, false, false, kModeBlse>(tq, tk, tv, p, num_sms, st);
+  return two ? launch_one<D, true, true, kModeSparse>(tq, tk, tv, p, num_sms, st)
+             : launch_one<D, false, false, kModeSparse>(tq, tk, tv, p, num_sms, st);
+}
+
 cudaError_t launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                        const AttnParams& p, int head_dim, bool two, bool sparse, int num_sms,
+                        const AttnParams& p, int head_dim, bool two, int mode, int num_sms,
                         cudaStream_t st) {
-  if (head_dim == 128) {
-    if (!sparse) return launch_one<128, false, false>(tq, tk, tv, p, num_sms, st);
-    return two ? launch_one<128, true, true>(tq, tk, tv, p, num_sms, st)
-               : launch_one<128, false, true>(tq, tk, tv, p, num_sms, st);
-  }
-  if (!sparse) return launch_one<64, false, false>(tq, tk, tv, p, num_sms, st);
-  return two ? launch_one<64, true, true>(tq, tk, tv, p, num_sms, st)
-             : launch_one<64, false, true>(tq, tk, tv, p, num_sms, st);
+  return head_dim == 128 ? launch_d<128>(tq, tk, tv, p, two, mode, num_sms, st)
+                         : launch_d<64>(tq, tk, tv, p, two, mode, num_sms, st);
 }
 
 }  // namespace adaspa

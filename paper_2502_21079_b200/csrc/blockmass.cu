@@ -1,0 +1,90 @@
+// blockmass.cu -- the second half of the fused search step t_w (Alg. 1):
+// block masses from the per-(row, kv block) log-sum-exps that the dense pass wrote (attn_fwd.cu,
+// kModeBlse), with the fresh LSE of the same pass:
+//
+//   block_mass[b,h,qb,kb] = sum_{i in qb} sum_{j in kb} exp(s_ij - lse_i)
+//                         = sum_{i in qb} 2^(blse[b,h,kb,i] - lrel[b,h,i])
+//
+// (W_sum_attn, reading R4.)  Both operands are relative to the same per-row
+// reference (the row's first running max), so their difference is formed from small numbers and
+// keeps fp32 precision.  No QK^T recompute and no second pass of exponentials over S: the dense
+// pass already computed every exp(s_ij - m_i); this kernel reads N*nb floats per head (HBM-bound)
+// and does one exponential per (row, kv block).
+#include "attn.cuh"
+#include "common.cuh"
+
+namespace adaspa {
+
+namespace {
+
+constexpr int kWarps = 8;
+
+// One CTA per (b, h, q-block): warp w takes kv blocks w, w+8, ...; lane l holds rows l + 32r of the
+// q-block (coalesced 128-byte loads along the token axis of blse[b,h,kb,:]); the q-block's mass row
+// is staged in shared memory and written contiguously.
+template <int R>
+__global__ void __launch_bounds__(kWarps * 32) block_mass_kernel(BlockMassParams p) {
+  extern __shared__ float mrow[];
+  const int nb = p.grid.nb;
+  const int qb = blockIdx.x % nb;
+  const int bhl = blockIdx.x / nb;
+  const int b = bhl / p.nh;
+  const int h = p.h0 + (bhl - b * p.nh);
+  const int start = p.grid.start(qb);
+  const int len = p.grid.len(qb);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float lr[R];
+  bool ok[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = lane + 32 * r;
+    ok[r] = i < len;
+    lr[r] = ok[r] ? __ldg(p.lrel + static_cast<int64_t>(bhl) * p.N + start + i) : 0.0f;
+  }
+  const float* base = p.blse + static_cast<int64_t>(bhl) * nb * p.N + start;
+  constexpr int U = 4;  // kv blocks in flight per warp
+  for (int kb0 = warp * U; kb0 < nb; kb0 += kWarps * U) {
+    float x[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int kb = kb0 + u;
+        x[u][r] = (kb < nb && ok[r]) ? __ldcs(base + static_cast<int64_t>(kb) * p.N + lane + 32 * r) : -INFINITY;
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc += ok[r] ? exp2f(x[u][r] - lr[r]) : 0.0f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0 && kb0 + u < nb) mrow[kb0 + u] = acc;
+    }
+  }
+  __syncthreads();
+  float* out = p.mass + ((static_cast<int64_t>(b) * p.H + h) * nb + qb) * nb;
+  for (int j = threadIdx.x; j < nb; j += kWarps * 32) out[j] = mrow[j];
+}
+
+}  // namespace
+
+cudaError_t launch_block_mass(const BlockMassParams& p, cudaStream_t st) {
+  const int64_t ctas = static_cast<int64_t>(p.B) * p.nh * p.grid.nb;
+  if (ctas <= 0) return cudaSuccess;
+  if (ctas > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(float) * p.grid.nb;
+  cudaError_t e;
+  if (p.grid.bs == 64) {
+    if ((e = cudaFuncSetAttribute(block_mass_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+      return e;
+    block_mass_kernel<2><<<static_cast<unsigned>(ctas), kWarps * 32, smem, st>>>(p);
+  } else {
+    if ((e = cudaFuncSetAttribute(block_mass_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+      return e;
+    block_mass_kernel<4><<<static_cast<unsigned>(ctas), kWarps * 32, smem, st>>>(p);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace adaspa

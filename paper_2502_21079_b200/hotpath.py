@@ -1,9 +1,12 @@
 """One pass of the AdaSpa hot path on fixed shapes:
 
-    K1 dense attention + LSE  ->  K2 block mass with that LSE  ->  K3 selection  ->  K4 sparse forward
+    search step t_w (Alg. 1):  K1 dense attention + LSE + block mass with that LSE  ->  K3 selection
+    every later step:          K4 block-sparse forward on the cached CSR
+    later key steps (Alg. 2):  K2 block mass with the cached LSE  ->  K3
 
-This is the search step t_w of the schedule (Alg. 1) followed by the
-block-sparse forward every later step runs.  Buffers are allocated once;
+`search(fused=True)` runs Alg. 1 as ONE dense pass that also emits per-(row, kv block)
+log-sum-exps plus an HBM-bound block-mass reduction (adaspa_dense_attn_lse_search);
+`search(fused=False)` runs it as K1 then K2 with the fresh LSE.  Buffers are allocated once;
 `run()` accepts device tensors or (pinned) host tensors, in which case it stages them to the
 device on the same stream; `run_sparse_host()` is a sparse step end to end from host memory.
 Everything runs through the C ABI; nothing here computes.
@@ -45,6 +48,8 @@ class HotPath:
         self.csr = L.Csr(e(rows + 1, dt=torch.int32), e(rows * self.nb, dt=torch.int32), e(rows, dt=torch.int32),
                          e(batch, heads, dt=torch.float32), e(batch, heads, dt=torch.int64))
         self.ws = e(max(L.sparse_workspace_bytes(self.desc), 1), dt=torch.uint8)
+        self.fws = None     # fused-search scratch (4*(nb+1)*N bytes per head), allocated on first use
+        self.mass2 = None   # block masses of a later key step (K2 with the cached LSE)
 
     def _stage(self, q, k, v):
         """Device tensors are used in place (any layout the descriptor strides can express, e.g. the
@@ -58,20 +63,45 @@ class HotPath:
         self.v.copy_(v, non_blocking=True)
         return self.q, self.k, self.v
 
-    def search(self, q, k, v, events=None):
-        """The search step t_w (Alg. 1): K1 dense attention + LSE, K2 block mass with that LSE, K3
-        selection into self.csr.  events: optional list of 4 CUDA events recorded around K1, K2, K3."""
+    def search(self, q, k, v, events=None, fused=True):
+        """The search step t_w (Alg. 1) into self.o_dense, self.lse (the LSE cache), self.mass and
+        self.csr.  fused: K1+K2 in one dense pass (adaspa_dense_attn_lse_search), else K1 then K2.
+        events: optional list of 4 CUDA events recorded around K1, K2, K3 (fused: the whole fused
+        call between events 0 and 1, nothing between 1 and 2)."""
         q, k, v = self._stage(q, k, v)
         rec = (lambda i: events[i].record()) if events else (lambda i: None)  # noqa: E731
         rec(0)
-        L.dense_attn_lse(q, k, v, o=self.o_dense, lse=self.lse, **self.kw)
-        rec(1)
-        L.lse_cached_search(q, k, self.lse, block_mass=self.mass, **self.kw)
+        if fused:
+            if self.fws is None:
+                self.fws = torch.empty(L.fused_search_workspace_bytes(self.desc, 0), dtype=torch.uint8,
+                                       device=self.device)
+            L.dense_attn_lse_search(q, k, v, o=self.o_dense, lse=self.lse, block_mass=self.mass,
+                                    workspace=self.fws, **self.kw)
+            rec(1)
+        else:
+            L.dense_attn_lse(q, k, v, o=self.o_dense, lse=self.lse, **self.kw)
+            rec(1)
+            L.lse_cached_search(q, k, self.lse, block_mass=self.mass, **self.kw)
         rec(2)
         L.select_blocks(self.mass, heads_desc=self.desc, mode=self.mode, target=self.targets, flags=self.flags,
                         tier_tau=self.tier_tau, out=self.csr)
         rec(3)
         return self.csr
+
+    def dense(self, q, k, v, o=None, lse=None):
+        """K1 alone (a warm-up step before t_w): O (and the LSE if `lse` is given)."""
+        q, k, v = self._stage(q, k, v)
+        o = self.o_dense if o is None else o
+        L.dense_attn_lse(q, k, v, o=o, lse=lse, want_lse=lse is not None, **self.kw)
+        return o
+
+    def cached_search(self, q, k):
+        """K2 of a later key step (Alg. 2): block masses with the CACHED t_w LSE
+        (self.lse, reading R19) into self.mass2."""
+        if self.mass2 is None:
+            self.mass2 = torch.empty_like(self.mass)
+        L.lse_cached_search(q, k, self.lse, block_mass=self.mass2, **self.kw)
+        return self.mass2
 
     def sparse(self, q, k, v, csr=None, o=None):
         """K4 on the cached index lists (self.csr unless given): the step every later denoising step runs."""
@@ -81,17 +111,17 @@ class HotPath:
         L.block_sparse_attn(q, k, v, csr.row_ptr, csr.col_idx, o=o, workspace=self.ws, **self.kw)
         return o
 
-    def run(self, q, k, v, events=None):
+    def run(self, q, k, v, events=None, fused=True):
         """search() then sparse(); events: optional list of 5 CUDA events recorded around K1..K4."""
         q, k, v = self._stage(q, k, v)
-        self.search(q, k, v, events=events[:4] if events else None)
+        self.search(q, k, v, events=events[:4] if events else None, fused=fused)
         self.sparse(q, k, v)
         if events:
             events[4].record()
         return self.o_sparse
 
-    # launches of our kernels per run(): K1 1, K2 1, K3 4 (rows, head, scan, write; +2 with tiers),
-    # K4 3 (stream + order + attention)
+    # launches of our kernels per run(): fused search 2 (dense pass + block mass; K1 + K2 unfused), K3 4
+    # (rows, head, scan, write; +2 with tiers), K4 3 (stream + order + attention)
     def kernels_per_run(self):
         return 9 + (2 if self.flags & L.FLAG_HEAD_TIERS else 0)
 

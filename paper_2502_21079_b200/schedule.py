@@ -2,7 +2,8 @@
 
 PAPER.md:397-405 (fig:overview caption): warm-up steps run full attention; the first key step
 t_key^1 = t_w runs the Fused Online Search (Alg. 1: dense attention that also emits the LSE, then
-the block mass with that fresh LSE); every later key step runs the LSE-Cached
+the block mass with that fresh LSE, PAPER.md:459-497 -- here one dense pass that also emits the
+per-(row, kv block) log-sum-exps, adaspa_dense_attn_lse_search, unless fused_search=False); every later key step runs the LSE-Cached
 Online Search (Alg. 2) with the LSE cached at t_w; all other steps after t_w run
 the head-adaptive block-sparse attention with the cached index lists.
 Defaults: T_s = {10, 30}, 10 warm-up steps, 50 steps.
@@ -68,7 +69,8 @@ class AdaSpaSchedule:
     """
 
     def __init__(self, *, block_size, n_text, text_first=False, n_steps=50, t_w=10, key_steps=(10, 30),
-                 mode=L.SELECT_RECALL, targets=0.9, flags=L.FLAG_TEXT_SINK, tier_tau=0.8, softmax_scale=0.0):
+                 mode=L.SELECT_RECALL, targets=0.9, flags=L.FLAG_TEXT_SINK, tier_tau=0.8, softmax_scale=0.0,
+                 fused_search=True, fused_heads_per_pass=0):
         self.kw = dict(block_size=block_size, n_text=n_text, text_first=text_first, softmax_scale=softmax_scale)
         self.n_steps, self.t_w = int(n_steps), int(t_w)
         self.key_steps = sorted(set(int(x) for x in key_steps))
@@ -77,6 +79,9 @@ class AdaSpaSchedule:
         self.targets = targets
         self.layers = {}
         self.calls = []  # (t, layer, mode) log, for tests and reports
+        self.fused_search = fused_search
+        self.fused_heads_per_pass = fused_heads_per_pass   # 0: all heads in one pass
+        self._fws = None   # fused-search scratch, shared by all layers (the library allocates nothing)
 
     def _targets(self, H):
         if isinstance(self.targets, (int, float)):
@@ -109,9 +114,20 @@ class AdaSpaSchedule:
         if mode == FULL:
             L.dense_attn_lse(q, k, v, o=o, want_lse=False, **self.kw)
         elif mode == FULL_SEARCH:
-            L.dense_attn_lse(q, k, v, o=o, lse=c.lse, **self.kw)   # λ from t_w becomes the cache (R19)
-            c.have_lse = True
-            self._search(c, desc, q, k)                              # Alg. 1 second pass, fresh λ
+            if self.fused_search:                                    # Alg. 1 in one dense pass
+                need = L.fused_search_workspace_bytes(desc, self.fused_heads_per_pass)
+                if self._fws is None or self._fws.numel() < need:
+                    self._fws = torch.empty(need, dtype=torch.uint8, device=q.device)
+                L.dense_attn_lse_search(q, k, v, o=o, lse=c.lse, block_mass=c.mass, workspace=self._fws,
+                                        **self.kw)                   # λ from t_w becomes the cache (R19)
+                c.have_lse = True
+                L.select_blocks(c.mass, heads_desc=desc, mode=self.mode, target=self._targets(desc.heads),
+                                flags=self.flags, tier_tau=self.tier_tau, out=c.csr)
+                c.have_mask = True
+            else:
+                L.dense_attn_lse(q, k, v, o=o, lse=c.lse, **self.kw)   # λ from t_w becomes the cache (R19)
+                c.have_lse = True
+                self._search(c, desc, q, k)                              # Alg. 1 second pass, fresh λ
         else:
             if not c.have_mask:
                 raise RuntimeError(f"layer {layer}: step {t} needs the mask of step t_w={self.t_w}")

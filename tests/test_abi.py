@@ -26,7 +26,7 @@ def lib():
 
 def test_exports_every_header_symbol(lib):
     names = _header_functions()
-    assert len(names) == 10, names
+    assert len(names) == 12, names
     for n in names:
         assert hasattr(lib._lib, n), n
         assert n in lib.SYMBOLS, n
@@ -109,3 +109,23 @@ def test_sparse_workspace_and_errors(lib):
     assert st == lib.ERR_INVALID_ARG
     st = L.adaspa_block_sparse_attn(ctypes.byref(d), fake, fake, fake, fake, fake, fake, nul, fake, 16, nul)
     assert st == lib.ERR_WORKSPACE_TOO_SMALL
+
+
+def test_fused_search_workspace_and_errors(lib):
+    """adaspa_dense_attn_lse_search: workspace sizing (4*(nb+1)*N bytes per head and batch element,
+    passes of as many heads as fit) and argument errors rejected before any launch."""
+    L = lib._lib
+    d = _desc(lib)
+    nb = lib.num_blocks(d)
+    per = 4 * (nb + 1) * d.seq_len * d.batch
+    assert lib.fused_search_workspace_bytes(d, 1) == per
+    assert lib.fused_search_workspace_bytes(d, 0) == per * d.heads
+    assert lib.fused_search_workspace_bytes(d, 99) == per * d.heads
+    fake = ctypes.c_void_p(0x10000)
+    nul = ctypes.c_void_p(0)
+    st = L.adaspa_dense_attn_lse_search(ctypes.byref(d), fake, fake, fake, fake, fake, fake, fake, per - 1, nul)
+    assert st == lib.ERR_WORKSPACE_TOO_SMALL
+    st = L.adaspa_dense_attn_lse_search(ctypes.byref(d), fake, fake, fake, fake, fake, nul, fake, per, nul)
+    assert st == lib.ERR_INVALID_ARG and b"block_mass" in L.adaspa_last_error()
+    st = L.adaspa_dense_attn_lse_search(ctypes.byref(d), nul, fake, fake, fake, fake, fake, fake, per, nul)
+    assert st == lib.ERR_INVALID_ARG

@@ -35,7 +35,8 @@ def ada():
 
 @pytest.mark.parametrize("edge", EDGES, ids=[e[0] for e in EDGES])
 @pytest.mark.parametrize("mode", ["recall", "sparsity"])
-def test_hot_path_edges(ada, edge, mode):
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "twopass"])
+def test_hot_path_edges(ada, edge, mode, fused):
     from paper_2502_21079_b200.hotpath import HotPath
     name, f, h, w, nt, tf, H, d, B, batch = edge
     lay = workloads.layout_for("tiny", f=f, h=h, w=w, n_text=nt, text_first=tf, heads=H, head_dim=d, block=B)
@@ -43,7 +44,7 @@ def test_hot_path_edges(ada, edge, mode):
     kmode = ada.SELECT_RECALL if mode == "recall" else ada.SELECT_SPARSITY
     target = 0.9 if mode == "recall" else 0.5
     hp = HotPath(batch, H, lay.n, d, B, nt, tf, mode=kmode, targets=target)
-    o = hp.run(q, k, v)
+    o = hp.run(q, k, v, fused=fused)
     torch.cuda.synchronize()
     blocks = oracle.block_map(lay.n_video, lay.n_text, B, tf)
     nb = len(blocks)

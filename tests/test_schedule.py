@@ -41,12 +41,13 @@ def test_trace_rejects_bad_key_steps():
 
 
 @pytest.mark.gpu
-def test_schedule_gpu_matches_oracle_pipeline():
+@pytest.mark.parametrize("fused", [True, False])
+def test_schedule_gpu_matches_oracle_pipeline(fused):
     from gpu_helpers import compare_out, csr_rows, np64, selection_ok
     lay = workloads.layout_for("tiny")
     n_steps, t_w, ks = 6, 2, [2, 4]
     sch = S.AdaSpaSchedule(block_size=lay.block, n_text=lay.n_text, text_first=lay.text_first,
-                           n_steps=n_steps, t_w=t_w, key_steps=ks, targets=0.9)
+                           n_steps=n_steps, t_w=t_w, key_steps=ks, targets=0.9, fused_search=fused)
     blocks = oracle.block_map(lay.n_video, lay.n_text, lay.block, lay.text_first)
     nb = len(blocks)
     scale = 1 / math.sqrt(lay.head_dim)

@@ -52,6 +52,14 @@ if "k2" in what:
     M = ada.lse_cached_search(q, k, lse, **kw)
     t = timeit(lambda: ada.lse_cached_search(q, k, lse, block_mass=M, **kw), 5)
     out["k2_ms"] = t
+if "fs" in what:
+    desc0 = ada.make_desc(q, lay.block, lay.n_text, lay.text_first)
+    nb = ada.num_blocks(desc0)
+    wsf = torch.empty(ada.fused_search_workspace_bytes(desc0, 0), dtype=torch.uint8, device="cuda")
+    Mf = torch.empty(1, H, nb, nb, dtype=torch.float32, device="cuda")
+    t = timeit(lambda: ada.dense_attn_lse_search(q, k, v, o=o, lse=lse, block_mass=Mf, workspace=wsf, **kw), 3)
+    out["fs_ms"] = t
+    del wsf
 if "k4" in what:
     desc = ada.make_desc(q, lay.block, lay.n_text, lay.text_first)
     ws = torch.empty(ada.sparse_workspace_bytes(desc), dtype=torch.uint8, device="cuda")
