@@ -17,7 +17,7 @@ for r in rows[1:]:
     agg.setdefault(name, []).append(float(r[iv].replace(",", "")) * scale)
 tot = sum(sum(v) for v in agg.values())
 lines = [f"# ncu launch list summary: {os.path.basename(src)}", "",
-         "`ncu --metrics gpu__time_duration.sum --clock-control none` over `python bench.py --steps 2 --warmup 3 "
+         "`ncu --metrics gpu__time_duration.sum --clock-control none` over `python tools/prof_fused.py <config>` (one fused search, one K1, one K2) "
          "--no-cpu-baseline --no-e2e` (HYV-110K). Per-launch times are cold-cache and serialised: compare shares.", "",
          "| kernel | launches | mean ms | share of our kernels |", "|---|---|---|---|"]
 for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
