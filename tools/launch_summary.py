@@ -16,9 +16,10 @@ for r in rows[1:]:
     scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "msecond": 1.0}.get(r[iu], 1e-6)
     agg.setdefault(name, []).append(float(r[iv].replace(",", "")) * scale)
 tot = sum(sum(v) for v in agg.values())
+desc = sys.argv[3] if len(sys.argv) > 3 else "python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e (HYV-110K)"
 lines = [f"# ncu launch list summary: {os.path.basename(src)}", "",
-         "`ncu --metrics gpu__time_duration.sum --clock-control none` over `python tools/prof_fused.py <config>` (one fused search, one K1, one K2) "
-         "--no-cpu-baseline --no-e2e` (HYV-110K). Per-launch times are cold-cache and serialised: compare shares.", "",
+         f"`ncu --metrics gpu__time_duration.sum --clock-control none` over `{desc}`. "
+         "Per-launch times are cold-cache and serialised: compare shares.", "",
          "| kernel | launches | mean ms | share of our kernels |", "|---|---|---|---|"]
 for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
     lines.append(f"| `{k}` | {len(v)} | {sum(v)/len(v):.4f} | {sum(v)/tot*100:.2f}% |")
