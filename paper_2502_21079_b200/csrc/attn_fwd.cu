@@ -182,6 +182,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr bool SPARSE = MODE == kModeSparse;
   constexpr bool GRID = MODE != kModeDense;  // kv tiles follow the block grid
   constexpr bool BLSE = MODE == kModeBlse;
+  // skip the exponentials of fully masked 64-column halves: only where they are common (the B=64
+  // pairs of the sparse stream); elsewhere the branch costs registers for nothing
+  constexpr bool kSkipDead = SPARSE && KVTWO;
   using S = Smem<D>;
   constexpr int NS = S::kNS;
   constexpr bool kSepP = D == 64;
@@ -811,6 +814,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t pk[16];
+        // a 64-column half masked for every row of the warp (a dropped quadrant of a B=64 pair, the
+        // empty half of an odd B=64 tail, a dense tail shorter than 64): P = 0 without exponentials
+        // (at d = 64 the MUFU is the bound, and these are ~18% of the tile work at CogX-45K)
+        const bool dead = kSkipDead && (c == 0 ? limA == 0 : limB <= 64);
+        if (dead) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = 0u;
+        } else {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int i = 32 * c + 4 * k;
@@ -835,6 +846,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           acc[(k & 1) * 2 + 1] = fadd2(acc[(k & 1) * 2 + 1], p1);
           pk[2 * k] = pack_bf16x2(p0.x, p0.y);
           pk[2 * k + 1] = pack_bf16x2(p1.x, p1.y);
+        }
         }
         tmem_st_16x128b_x8(p_addr + c * 32, pk);
         if (c == 0) {  // first half of P stored: the MMA thread may start PV on kv rows 0-63

@@ -46,6 +46,30 @@ def compare_out(o_gpu, o_ref, lse_gpu=None, lse_ref=None, what=""):
     return d.max(), d.mean()
 
 
+def selection_ok_topk(masses, forced, candidates, k, gpu_kept, oracle_kept):
+    """The tie-zone rule for SPARSITY mode (row-wise top-k; R6/R10-R12): the
+    GPU keeps the forced set plus exactly k candidates, and (G xor O) lies among candidates whose
+    normalised mass is within 1e-6 of the k-th largest (the cut), where several top-k sets exist."""
+    m = np.asarray(masses, dtype=np.float64)
+    T = m.sum()
+    G, O = set(gpu_kept), set(oracle_kept)
+    if not set(forced) <= G:
+        return False, "forced blocks missing"
+    kk = min(k, len(candidates))
+    if len(G - set(forced)) != kk:
+        return False, f"{len(G - set(forced))} candidates kept, want {kk}"
+    if G == O:
+        return True, ""
+    mh = m / T if T > 0 else m
+    order = sorted(candidates, key=lambda j: (-m[j], j))
+    c = mh[order[kk - 1]] if kk > 0 else 0.0
+    A = {j for j in candidates if abs(mh[j] - c) <= TIE}
+    diff = G ^ O
+    if not diff <= A:
+        return False, f"diff {sorted(diff)} not in tie zone {sorted(A)}"
+    return True, ""
+
+
 def selection_ok(masses, forced, candidates, r, gpu_kept, oracle_kept):
     """north_star tie-zone rule: (G xor O) must lie in the ambiguity set A,
     and G must still reach the recall target (within 1e-6)."""

@@ -11,7 +11,7 @@ import torch
 
 import oracle
 import workloads
-from gpu_helpers import MASS_REL, compare_out, csr_rows, np64, selection_ok
+from gpu_helpers import MASS_REL, compare_out, csr_rows, np64, selection_ok, selection_ok_topk
 
 pytestmark = pytest.mark.gpu
 
@@ -68,8 +68,10 @@ def test_hot_path_edges(ada, edge, mode, fused):
                     good, msg = selection_ok(M[p], forced, cands, target, got, exp)
                     assert good, f"{name} b{b} h{hh} row {p}: {msg}"
                 else:
-                    exp = oracle.select_row_sparsity(M[p], forced, cands, oracle.k_from_sparsity(target, n_video_blocks))
-                    assert len(got) == len(exp), f"{name} b{b} h{hh} row {p}: {got} vs {exp}"
+                    kk = oracle.k_from_sparsity(target, n_video_blocks)
+                    exp = oracle.select_row_sparsity(M[p], forced, cands, kk)
+                    good, msg = selection_ok_topk(M[p], forced, cands, kk, got, exp)
+                    assert good, f"{name} b{b} h{hh} row {p}: {msg}"
                 assert got, "no row may be empty"
             kept = [rows[(b * H + hh) * nb + p] for p in range(nb)]
             so, _ = oracle.masked_attention(qq, kk, vv, blocks, kept, scale)

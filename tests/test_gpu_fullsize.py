@@ -74,3 +74,53 @@ def test_fullsize_hot_path_sampled(ada, name):
             assert good, f"{name} K3 h{h} qb{p}: {msg}"
             so, _ = oracle.masked_attention(qh, kh, vh, blocks, {p: g_sel}, scale, q_block_ids=[p])  # a4
             compare_out(o[0, h, rows], so, what=f"{name} K4 h{h} qb{p}")
+
+
+@pytest.mark.parametrize("name", ["cogx45k", "hyv110k"])
+def test_fullsize_sparsity_tiers(ada, name):
+    """The paper's default selection at full size: SPARSITY 0.8 with
+    head-adaptive tiers and the text sink.  K3 on the GPU's block masses equals the oracle's selection
+    on the same masses for EVERY row (tiers need every row: head Recall over the whole matrix, then
+    n = min(#{R_h > 0.8}, H/2) heads raised / lowered); the per-head kept counts and Recalls agree;
+    sampled rows are also checked against the oracle's OWN masses (sparsity tie-zone rule)."""
+    from gpu_helpers import selection_ok_topk
+    from paper_2502_21079_b200.hotpath import HotPath
+    lay = workloads.layout_for(name)
+    q, k, v = workloads.generate_qkv(lay, device="cuda")
+    hp = HotPath(1, lay.heads, lay.n, lay.head_dim, lay.block, lay.n_text, lay.text_first,
+                 mode=ada.SELECT_SPARSITY, targets=0.8, flags=ada.FLAG_TEXT_SINK | ada.FLAG_HEAD_TIERS)
+    hp.search(q, k, v)
+    torch.cuda.synchronize()
+    blocks = oracle.block_map(lay.n_video, lay.n_text, lay.block, lay.text_first)
+    nb = len(blocks)
+    H = lay.heads
+    Mg = hp.mass[0].double().cpu().numpy()
+    keep, rec, nnz, s_h = oracle.select_blocks(Mg, blocks, "sparsity", [0.8] * H, text_sink=True, tiers=True)
+    assert sorted(set(np.round(s_h, 12))) != [0.8], "no head was re-tiered"
+    rp = hp.csr.row_ptr.cpu().numpy()
+    ci = hp.csr.col_idx.cpu().numpy()
+    for h in range(H):
+        for p in range(nb):
+            row = h * nb + p
+            assert ci[rp[row]:rp[row + 1]].tolist() == np.nonzero(keep[h, p])[0].tolist(), (name, h, p)
+    np.testing.assert_array_equal(hp.csr.head_nnz[0].cpu().numpy(), nnz)
+    np.testing.assert_allclose(hp.csr.head_recall[0].cpu().numpy(), rec, rtol=1e-6)
+    # sampled rows against the oracle's own masses
+    scale = 1.0 / math.sqrt(lay.head_dim)
+    rng = np.random.default_rng(11)
+    n_cand = sum(1 for b in blocks if b.modality == "video")
+    for h in sorted({int(np.argmax(s_h)), int(np.argmin(s_h))}):
+        qh, kh = np64(q[0, h]), np64(k[0, h])
+        for p in _sample_blocks(blocks, rng, n_random=1):
+            b = blocks[p]
+            rows = slice(b.start, b.start + b.length)
+            _, lse = oracle.dense_attention(qh[rows], kh, np64(v[0, h]), scale)
+            lse_full = np.zeros(lay.n)
+            lse_full[rows] = lse
+            M = oracle.block_mass(qh, kh, lse_full, blocks, scale, q_block_ids=[p])[0]
+            forced, cands = oracle.row_forced_and_candidates(blocks, p, True)
+            kk = oracle.k_from_sparsity(s_h[h], n_cand)
+            exp = oracle.select_row_sparsity(M, forced, cands, kk)
+            row = h * nb + p
+            good, msg = selection_ok_topk(M, forced, cands, kk, ci[rp[row]:rp[row + 1]].tolist(), exp)
+            assert good, f"{name} h{h} qb{p} (s={s_h[h]}): {msg}"

@@ -135,11 +135,11 @@ def test_select_blocks_exact(ada, tf, mode):
     assert (np.diff(cnt[order]) <= 0).all()
 
 
-@pytest.mark.parametrize("nv,nt", [(70000, 226), (150000, 256), (261000, 256)])
+@pytest.mark.parametrize("nv,nt", [(70000, 226), (150000, 256), (261000, 256), (349000, 256), (392900, 256)])
 @pytest.mark.parametrize("mode", ["recall", "sparsity"])
 def test_select_blocks_exact_large_nb(ada, nv, nt, mode):
-    """K3 at nb > 1024 (more than 32 kv-blocks per warp lane: nb = 1098 / 2348 / 4082 at block 64,
-    the range the length sweep reaches); sampled rows (every text row, the first and last video
+    """K3 at nb > 1024 (more than 32 kv-blocks per warp lane: nb = 1098 / 2348 / 4082 at block 64, and
+    the KPL=192 instantiation at nb = 5458 (the 24 s length-sweep point) and 6144 (the limit)); sampled rows (every text row, the first and last video
     rows, seeded random rows) bit-exact against the oracle's per-row selection."""
     H, B = 2, 64
     blocks = oracle.block_map(nv, nt, B, False)

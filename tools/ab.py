@@ -21,7 +21,7 @@ import workloads
 import paper_2502_21079_b200 as ada
 from paper_2502_21079_b200.hotpath import HotPath
 from bench import kept_flops
-lay = workloads.layout_for(%(config)r)
+lay = workloads.layout_for(%(config)r, **%(over)r)
 q, k, v = workloads.generate_qkv(lay, device="cuda")
 kw = dict(block_size=lay.block, n_text=lay.n_text, text_first=lay.text_first)
 N, H, d = lay.n, lay.heads, lay.head_dim
@@ -75,15 +75,17 @@ def main():
     ap.add_argument("--config", default="hyv110k")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--what", default="k1,k4")
+    ap.add_argument("--block", type=int, default=0, help="override the config's block size")
     a = ap.parse_args()
-    csr = f"/tmp/ab_csr_{a.config}.pt"
+    over = {"block": a.block} if a.block else {}
+    csr = f"/tmp/ab_csr_{a.config}_{a.block}.pt"
     if os.path.exists(csr):
         os.unlink(csr)
     res = {lib: [] for lib in a.libs}
     for r in range(a.reps):
         for lib in a.libs:
             env = dict(os.environ, ADASPA_LIB=os.path.abspath(lib))
-            code = CHILD % dict(root=ROOT, config=a.config, csr=csr, what=a.what)
+            code = CHILD % dict(root=ROOT, config=a.config, csr=csr, what=a.what, over=over)
             p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
             line = [x for x in p.stdout.splitlines() if x.startswith("RESULT ")]
             if p.returncode or not line:
