@@ -68,9 +68,9 @@ def test_hot_path_edges(ada, edge, mode, fused):
                     good, msg = selection_ok(M[p], forced, cands, target, got, exp)
                     assert good, f"{name} b{b} h{hh} row {p}: {msg}"
                 else:
-                    kk = oracle.k_from_sparsity(target, n_video_blocks)
-                    exp = oracle.select_row_sparsity(M[p], forced, cands, kk)
-                    good, msg = selection_ok_topk(M[p], forced, cands, kk, got, exp)
+                    k_top = oracle.k_from_sparsity(target, n_video_blocks)
+                    exp = oracle.select_row_sparsity(M[p], forced, cands, k_top)
+                    good, msg = selection_ok_topk(M[p], forced, cands, k_top, got, exp)
                     assert good, f"{name} b{b} h{hh} row {p}: {msg}"
                 assert got, "no row may be empty"
             kept = [rows[(b * H + hh) * nb + p] for p in range(nb)]
