@@ -73,13 +73,18 @@ __device__ __forceinline__ uint32_t o_col(int t) { return 256u + static_cast<uin
 template <int D>
 __device__ __forceinline__ uint32_t p_col(int t) { return D == 64 ? o_col(t) + 64u : s_col(t); }
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// One exp group in ADASPA_EXP_POLY_MOD on an FMA-pipe polynomial instead of MUFU.EX2 (0: none).
+// Round 1 measured 1 in 8 best; after the round-1 softmax changes (16-row warps, vote-gated max) the
+// MUFU is no longer the limit and the polynomial's ~6 instructions per element cost more than they
+// relieve: A/B on one box (profiles/r02_ab_poly.txt) K1 1106 -> 1145 (d=128), 764 -> 805 (d=64),
+// K4 1007 -> 1044 TFLOP/s with none.  (K2 keeps its 1 pair in 8: 83.6 vs 85.2 ms, 22.9 vs 26.2.)
 #ifndef ADASPA_EXP_POLY_MOD
-#define ADASPA_EXP_POLY_MOD 8
+#define ADASPA_EXP_POLY_MOD 0
 #endif
 #ifndef ADASPA_ABLATE
 #define ADASPA_ABLATE 0  // diagnostic builds only: 4 = no softmax (MMA / TMA pipeline alone)
 #endif
-constexpr int kExpPolyMod = ADASPA_EXP_POLY_MOD;  // one group in kExpPolyMod on the FMA-pipe polynomial (0: none; 8 measured best)
+constexpr int kExpPolyMod = ADASPA_EXP_POLY_MOD;
 
 enum : int { kNormal = 0, kEnd = 1, kAllEnd = 2 };
 

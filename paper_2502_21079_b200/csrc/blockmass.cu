@@ -40,27 +40,37 @@ __global__ void __launch_bounds__(kWarps * 32) block_mass_kernel(BlockMassParams
     const int i = lane + 32 * r;
     ok[r] = i < len;
     lr[r] = ok[r] ? __ldg(p.lrel + static_cast<int64_t>(bhl) * p.N + start + i) : 0.0f;
+    if (!(lr[r] > -INFINITY)) ok[r] = false;  // an empty row (cannot occur in a dense pass) adds nothing
   }
   const float* base = p.blse + static_cast<int64_t>(bhl) * nb * p.N + start;
-  constexpr int U = 4;  // kv blocks in flight per warp
+  constexpr int U = 4;  // kv blocks in flight per warp (the reduction below assumes 4)
+  const int64_t Nl = p.N;
   for (int kb0 = warp * U; kb0 < nb; kb0 += kWarps * U) {
     float x[U][R];
+    const float* src = base + kb0 * Nl + lane;
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int kb = kb0 + u;
-        x[u][r] = (kb < nb && ok[r]) ? __ldcs(base + static_cast<int64_t>(kb) * p.N + lane + 32 * r) : -INFINITY;
-      }
+      for (int r = 0; r < R; ++r)
+        x[u][r] = (kb0 + u < nb && ok[r]) ? __ldcs(src + u * Nl + 32 * r) : -INFINITY;
+    float v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      float acc = 0.0f;
+      v[u] = 0.0f;
 #pragma unroll
-      for (int r = 0; r < R; ++r) acc += ok[r] ? exp2f(x[u][r] - lr[r]) : 0.0f;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0 && kb0 + u < nb) mrow[kb0 + u] = acc;
+      for (int r = 0; r < R; ++r) v[u] += ex2_approx(x[u][r] - lr[r]);  // invalid rows: -inf -> 0
     }
+    // transpose-reduce of the 4 per-lane sums over the warp: 6 shuffles instead of 4 x 5; lane
+    // 8*i ends with the sum of kv block kb0 + i
+    const bool hi16 = lane & 16, hi8 = lane & 8;
+    const float a0 = (hi16 ? v[2] : v[0]) + __shfl_xor_sync(0xffffffffu, hi16 ? v[0] : v[2], 16);
+    const float a1 = (hi16 ? v[3] : v[1]) + __shfl_xor_sync(0xffffffffu, hi16 ? v[1] : v[3], 16);
+    float c = (hi8 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, hi8 ? a0 : a1, 8);
+    c += __shfl_xor_sync(0xffffffffu, c, 4);
+    c += __shfl_xor_sync(0xffffffffu, c, 2);
+    c += __shfl_xor_sync(0xffffffffu, c, 1);
+    const int kb = kb0 + (lane >> 3);
+    if ((lane & 7) == 0 && kb < nb) mrow[kb] = c;
   }
   __syncthreads();
   float* out = p.mass + ((static_cast<int64_t>(b) * p.H + h) * nb + qb) * nb;

@@ -1,6 +1,9 @@
 """Summarise `ncu --set full` reports into profiles/ (markdown table + ncu_traffic.json for bench.py).
 
     python tools/ncu_summary.py TAG K1=gpurun_out/a.ncu-rep K2=... K3=... K4=...
+    python tools/ncu_summary.py TAG K1=gpurun_out/x.raw.csv@0 FS=gpurun_out/x.raw.csv@1 ...
+
+A `.raw.csv` (ncu -i rep --page raw --csv, exported on the GPU box) with `@i` picks its i-th launch.
 
 traffic = dram__bytes_read.sum + dram__bytes_write.sum per launch (bench.py's roofline.traffic).
 """
@@ -31,9 +34,16 @@ KEYS = [
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
-    h, units, vals = rows[0], rows[1], rows[2]
+    idx = 0
+    if "@" in rep:
+        rep, idx = rep.rsplit("@", 1)
+        idx = int(idx)
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = [r for r in csv.reader(io.StringIO(out)) if len(r) > 5]
+    h, units, vals = rows[0], rows[1], rows[2 + idx]
     d = {}
     for k, u, v in zip(h, units, vals):
         d[k] = (v, u)
@@ -45,7 +55,8 @@ def main():
     tag = sys.argv[1]
     items = [a.split("=", 1) for a in sys.argv[2:]]
     lines = [f"# ncu --set full summary ({tag})", "",
-             "One launch per kernel, `ncu --set full --clock-control none` on HYV-110K (tools/prof_one.py); "
+             "One launch per kernel, `ncu --set full --clock-control none` (tools/gpu_ncu_step.sh over "
+             "tools/prof_step.py, or tools/prof_one.py for r01 tags); "
              "cold-cache, serialised replays: use for shares and counters, not for bench values.", ""]
     traffic = {}
     table = {}
@@ -54,8 +65,8 @@ def main():
         d, kname = raw(rep)
         names[key] = kname
         table[key] = d
-        rd = float(d.get("dram__bytes_read.sum", ("0", ""))[0].replace(",", "") or 0)
-        wr = float(d.get("dram__bytes_write.sum", ("0", ""))[0].replace(",", "") or 0)
+        rd = float(d.get("dram__bytes_read.sum", ("0", ""))[0].replace(",", "").replace("-nan", "nan") or 0)
+        wr = float(d.get("dram__bytes_write.sum", ("0", ""))[0].replace(",", "").replace("-nan", "nan") or 0)
         unit_r = d.get("dram__bytes_read.sum", ("", "byte"))[1]
         unit_w = d.get("dram__bytes_write.sum", ("", "byte"))[1]
         mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -76,7 +87,7 @@ def main():
         f.write("\n".join(lines) + "\n")
     tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     old = json.load(open(tj)) if os.path.exists(tj) else {}
-    old.update({k: round(v) for k, v in traffic.items()})
+    old.update({k: round(v) for k, v in traffic.items() if v == v})
     old["_source"] = f"tools/ncu_summary.py {tag}: dram__bytes_read.sum + dram__bytes_write.sum per launch"
     json.dump(old, open(tj, "w"), indent=1)
     print("\n".join(lines))

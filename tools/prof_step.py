@@ -1,0 +1,30 @@
+"""One bench step on a BASELINE config for ncu captures (diagnostic; not the bench contract):
+K1 alone, the fused search (dense BLSE pass + block mass), K3, K4, K2 with the cached LSE -- the
+kernels in that launch order (attn_fwd_kernel: dense, then BLSE, then sparse).
+
+    python tools/prof_step.py [config] [runs]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import workloads
+import paper_2502_21079_b200 as ada
+from paper_2502_21079_b200.hotpath import HotPath
+
+name = sys.argv[1] if len(sys.argv) > 1 else "hyv110k"
+runs = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+lay = workloads.layout_for(name)
+q, k, v = workloads.generate_qkv(lay, device="cuda")
+hp = HotPath(1, lay.heads, lay.n, lay.head_dim, lay.block, lay.n_text, lay.text_first,
+             mode=ada.SELECT_RECALL, targets=0.9, flags=ada.FLAG_TEXT_SINK)
+o = torch.empty_like(q)
+for _ in range(runs):
+    hp.dense(q, k, v, o=o)
+    hp.search(q, k, v)
+    hp.sparse(q, k, v)
+    hp.cached_search(q, k)
+torch.cuda.synchronize()
+print("done", name, runs)
