@@ -281,11 +281,13 @@ def kernel_entries(lay, nb, nnz, kfl, med, peaks, traffic, p90=None, heads=None)
     if med.get("FS"):
         # algorithmic work of the fused search = the dense pass's 4N^2dH: the block masses reuse its
         # exponentials (no second QK^T); plus the block-LSE bytes written and read (4*(nb+1)*N per head)
-        out["K1K2_fused_search"] = roofline_entry(
+        out["K1K2K3_search_step"] = roofline_entry(
             "tensor", dense_fl / (med["FS"] / 1e3) / 1e12, tens_peak, "TFLOP/s", traffic.get("FS"),
             ms=rnd(med["FS"]), ms_p90=rnd(p90.get("FS")),
             blse_gb=round(2 * 4.0 * (nb + 1) * N * H / 1e9, 3),
-            note="dense pass + block LSEs (attn_fwd_kernel kModeBlse) then block_mass_kernel, one C-ABI call")
+            note="the whole search step t_w in one C-ABI call (adaspa_search_select): dense pass + block "
+                 "LSEs (attn_fwd_kernel kModeBlse), block_mass_kernel with the per-row RECALL selection "
+                 "epilogue, CSR assembly (head / scan / write)")
     out["K2_lse_cached_search"] = roofline_entry("alu", N * N * H / (med["K2"] / 1e3) / 1e12, exp_peak, "Texp/s",
                                                  traffic.get("K2"), ms=rnd(med["K2"]), ms_p90=rnd(p90.get("K2")),
                                                  tensor_tflops=round(dense_fl / 2 / (med["K2"] / 1e3) / 1e12, 1))
@@ -350,10 +352,14 @@ def variant_config(name, args, peaks, traffic, reps=5):
         rec = (lambda i: ev[i].record()) if ev else (lambda i: None)  # noqa: E731
         rec(0)
         hp.dense(q, k, v, o=o_warm)
-        hp.search(q, k, v, events=[ev[1], ev[2], ev[6], ev[3]] if ev else None, fused=True)
+        rec(1)
+        hp.search(q, k, v, fused=True)
+        rec(2)
         hp.sparse(q, k, v)
+        rec(3)
+        m2 = hp.cached_search(q, k)
         rec(4)
-        hp.cached_search(q, k)
+        hp.select(m2)
         rec(5)
 
     for _ in range(2):
@@ -363,18 +369,18 @@ def variant_config(name, args, peaks, traffic, reps=5):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
         one(ev)
         torch.cuda.synchronize()
-        per.append({"K1": ev[0].elapsed_time(ev[1]), "FS": ev[1].elapsed_time(ev[2]), "K3": ev[6].elapsed_time(ev[3]),
-                    "K4": ev[3].elapsed_time(ev[4]), "K2": ev[4].elapsed_time(ev[5])})
+        per.append({"K1": ev[0].elapsed_time(ev[1]), "FS": ev[1].elapsed_time(ev[2]), "K4": ev[2].elapsed_time(ev[3]),
+                    "K2": ev[3].elapsed_time(ev[4]), "K3": ev[4].elapsed_time(ev[5])})
     med = {n: stats([p[n] for p in per])[0] for n in per[0]}
     kfl, nnz = kept_flops(lay, hp.csr, lay.head_dim)
     kern = kernel_entries(lay, hp.nb, nnz, kfl, med, peaks, traffic.get(name, {}))
     out = {"seq_len": lay.n, "heads": lay.heads, "head_dim": lay.head_dim, "block": lay.block,
            "selection": f"recall {args.recall} per head, text sink",
            "K4_tflops": kern["K4_block_sparse_attn"]["achieved"], "ms_per_layer_sparse": round(med["K4"], 3),
-           "search_overhead_ms": round(med["FS"] - med["K1"] + med["K3"], 3),
-           "search_overhead_vs_dense": round((med["FS"] - med["K1"] + med["K3"]) / med["K1"], 4),
+           "search_overhead_ms": round(med["FS"] - med["K1"], 3),
+           "search_overhead_vs_dense": round((med["FS"] - med["K1"]) / med["K1"], 4),
            "search_overhead_cached_vs_dense": round((med["K2"] + med["K3"]) / med["K1"], 4),
-           "t_w_step_ms": {"fused": round(med["FS"] + med["K3"], 3),
+           "t_w_step_ms": {"fused_one_call": round(med["FS"], 3),
                            "two_pass_k1_k2_k3": round(med["K1"] + med["K2"] + med["K3"], 3)},
            "dense_ms": round(med["K1"], 3),
            "kept_density": round(nnz / (lay.heads * hp.nb * hp.nb), 4), "kernels": kern}
@@ -438,35 +444,41 @@ def run_ours(args):
     lse_warm = torch.empty(1, Hl, N, dtype=torch.float32, device=dev)
 
     # One step exercises every row of the path, in schedule order:
-    #   K1 (a warm-up step: dense attention + LSE) | fused search at t_w (K1 + K2 with the fresh LSE in
-    #   one dense pass, then the block-mass reduction) | K3 | [--lpt: CSR exchange] | K4 (a sparse step
-    #   on the cached CSR) | K2 (a later key step: block masses with the cached t_w LSE, Alg. 2)
-    # events: 0 K1 1 fused 2 (2b) K3 3 exchange 4 K4 5 K2 6
+    #   K1 (a warm-up step: dense attention + LSE) | the search step t_w in one C-ABI call
+    #   (adaspa_search_select: the dense pass with block LSEs, the block masses with the fresh LSE and,
+    #   per q-block row in the same CTA, the RECALL selection; then the CSR) | [--lpt: CSR exchange] |
+    #   K4 (a sparse step on the cached CSR) | K2 + K3 (a later key step: block masses with the cached
+    #   t_w LSE, Alg. 2, then the selection on them)
+    # events: 0 K1 1 t_w 2 exchange 3 K4 4 K2 5 K3 6
     def step(ev=None):
         rec = (lambda i: ev[i].record()) if ev else (lambda i: None)  # noqa: E731
         rec(0)
         hp.dense(q, k, v, o=o_warm, lse=lse_warm)
-        hp.search(q, k, v, events=[ev[1], ev[2], ev[7], ev[3]] if ev else None, fused=True)
+        rec(1)
+        hp.search(q, k, v, fused=True)
+        rec(2)
         if args.lpt:
             rp, ci = D.gather_csr(hp.csr.row_ptr, hp.csr.col_idx)
             prp, pci = D.pack_heads_csr(rp, ci, mine, nb)
-            rec(4)
+            rec(3)
             ada.block_sparse_attn(q4, k4, v4, prp, pci, block_size=lay.block, n_text=lay.n_text,
                                   text_first=lay.text_first, o=o4, workspace=ws4)
             step.csr = _Csr(prp, pci)
         else:
-            rec(4)
+            rec(3)
             hp.sparse(q, k, v)
             step.csr = hp.csr
+        rec(4)
+        m2 = hp.cached_search(q, k)
         rec(5)
-        hp.cached_search(q, k)
+        hp.select(m2)
         rec(6)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(K)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(K)]
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -479,16 +491,16 @@ def run_ours(args):
     if ws > 1:
         torch.distributed.barrier()
     clocks = clk.stop()
-    # per step: K1, fused search, K3, exchange, K4, K2 (cached LSE), total -- each the max over ranks
+    # per step: K1, t_w search step, exchange, K4, K2 (cached LSE), K3, total -- each the max over ranks
     NP = 7
-    per = [[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[7].elapsed_time(e[3]), e[3].elapsed_time(e[4]),
+    per = [[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]), e[3].elapsed_time(e[4]),
             e[4].elapsed_time(e[5]), e[5].elapsed_time(e[6]), e[0].elapsed_time(e[6])] for e in ev]
     flat = D.reduce_max([x for p in per for x in p])
     per = [flat[NP * s:NP * s + NP] for s in range(K)]
     tot = [sum(p[i] for p in per) for i in range(NP)]
     med = [stats([p[i] for p in per])[0] for i in range(NP)]
     p90 = [stats([p[i] for p in per])[1] for i in range(NP)]
-    I_K1, I_FS, I_K3, I_X, I_K4, I_K2, I_TOT = range(NP)
+    I_K1, I_FS, I_X, I_K4, I_K2, I_K3, I_TOT = range(NP)
     kfl, nnz = kept_flops(lay, step.csr, d)
     kfl_all, nnz_all = D.reduce_sum([kfl, nnz])
     value = kfl_all * K / (tot[I_K4] / 1e3) / 1e12
@@ -531,7 +543,7 @@ def run_ours(args):
 
     peaks, src = load_peaks()
     traffic = load_traffic()
-    launches = (hp.kernels_per_run() + 2) * K   # + K1 alone and K2 (cached LSE) per step
+    launches = (hp.kernels_per_run() + 2 + 4) * K   # + K1 alone, K2 (cached LSE) and K3 (4) per step
     variants = None
     if ws == 1 and not args.no_variants and args.config == "hyv110k":
         variants = {"hyv110k_sparsity0.8_tiers": variant_tiers(hp, q, k, v, lay, peaks)}
@@ -575,13 +587,14 @@ def run_ours(args):
                                    if ws > 1 else "1 GPU, whole layer"),
                    "l2": "inputs larger than L2 (Q,K,V = %.2f GB per layer)" % (3 * N * H * d * 2 / 1e9)},
         "ms_per_layer_sparse": round(ms[I_K4], 3),
-        # search overhead at t_w: what the fused search adds to a dense pass, plus K3
-        "search_overhead_ms": round(ms[I_FS] - ms[I_K1] + ms[I_K3], 3),
-        "search_overhead_vs_dense": round((tot[I_FS] - tot[I_K1] + tot[I_K3]) / tot[I_K1], 4),
+        # search overhead at t_w: what the whole search step (one call, selection included) adds to a
+        # dense pass
+        "search_overhead_ms": round(ms[I_FS] - ms[I_K1], 3),
+        "search_overhead_vs_dense": round((tot[I_FS] - tot[I_K1]) / tot[I_K1], 4),
         # at a later key step (Alg. 2: no dense pass runs; K2 with the cached LSE, then K3)
         "search_overhead_cached_ms": round(ms[I_K2] + ms[I_K3], 3),
         "search_overhead_cached_vs_dense": round((tot[I_K2] + tot[I_K3]) / tot[I_K1], 4),
-        "t_w_step_ms": {"fused": round(ms[I_FS] + ms[I_K3], 3),
+        "t_w_step_ms": {"fused_one_call": round(ms[I_FS], 3),
                         "two_pass_k1_k2_k3": round(ms[I_K1] + ms[I_K2] + ms[I_K3], 3)},
         "dense_ms": round(ms[I_K1], 3),
         "kept_density": round(nnz_all / (H * nb * nb), 4),
@@ -693,7 +706,8 @@ def run_ulysses(args):
     torch.cuda.synchronize()
     dist.barrier()
     clocks = clk.stop()
-    # phases: a2a in (search), K1, K2, K3, a2a out (search O), exchange, a2a in (sparse), K4, a2a out
+    # phases: a2a in (search), the search step (one call: dense pass, block masses + selection, CSR;
+    # phases 2-3 are empty then), a2a out (search O), exchange, a2a in (sparse), K4, a2a out
     per = [[e[i].elapsed_time(e[i + 1]) for i in range(9)] for e in evs]
     flat = D.reduce_max([x for p in per for x in p])
     per = [flat[9 * s:9 * s + 9] for s in range(K)]
@@ -712,8 +726,7 @@ def run_ulysses(args):
                        "head_dim": d, "block": lay.block,
                        "parallelism": f"ulysses a2a x{ws} (NCCL)" + (" + LPT sparse-step head sets" if args.lpt else ""),
                        "l2": "inputs larger than L2"},
-            "ms_per_layer_sparse": round(ms[7], 3), "t_w_fused_search_ms": round(ms[1], 3),
-            "k3_ms": round(ms[3], 3),
+            "ms_per_layer_sparse": round(ms[7], 3), "t_w_search_step_ms": round(ms[1] + ms[2] + ms[3], 3),
             "a2a_ms": {"search_in": round(ms[0], 3), "search_out": round(ms[4], 3), "sparse_in": round(ms[6], 3),
                        "sparse_out": round(ms[8], 3)},
             "exchange_ms": round(ms[5], 3),

@@ -14,6 +14,10 @@
  *
  *   adaspa_dense_attn_lse_search  K1+K2  dense forward + LSE + block mass
  *
+ * and the whole RECALL-mode search step t_w (f1 with its fused selection epilogue):
+ *
+ *   adaspa_search_select      K1+K2+K3  dense forward + LSE + block mass + CSR
+ *
  * Conventions (all functions):
  *  - Plain pointers only.  Every tensor argument is a DEVICE pointer owned by
  *    the caller unless its comment says "host".  The library allocates no
@@ -143,6 +147,34 @@ adaspa_status adaspa_dense_attn_lse_search(const adaspa_attn_desc* desc, const v
 /* Workspace bytes of adaspa_dense_attn_lse_search for passes of `heads_per_pass`
  * heads (<= 0 or > H: all heads in one pass). */
 size_t adaspa_fused_search_workspace_bytes(const adaspa_attn_desc* desc, int32_t heads_per_pass);
+
+/*
+ * K1+K2+K3 fused -- the whole search step t_w in RECALL mode (Alg. 1, PAPER.md:459-497,
+ * with the selection of PAPER.md:228-232 per q-block row; the fused RECALL epilogue of
+ * SURVEY.md 8(f) f1): the dense pass of adaspa_dense_attn_lse_search, then per q-block
+ * row the block masses with the fresh LSE AND that row's selection in the same CTA (the
+ * mass row is selected from shared memory; it is not re-read from HBM), then the CSR.
+ *   o, lse      as adaspa_dense_attn_lse (lse may be NULL);
+ *   block_mass  fp32 [B,H,nb,nb] output, or NULL (not written) when nb <= 2048; for
+ *               nb > 2048 it is required (the selection then runs as K3's row kernel on it);
+ *   recall      HOST double[H]: r_h, as adaspa_select_blocks in ADASPA_SELECT_RECALL mode;
+ *   flags       ADASPA_FLAG_TEXT_SINK or 0 (head tiers are a SPARSITY-mode rule: rejected);
+ *   row_ptr, col_idx, col_capacity, row_order, head_recall, head_nnz: as
+ *               adaspa_select_blocks -- bit-identical to adaspa_select_blocks on block_mass.
+ * workspace: >= adaspa_search_select_workspace_bytes(desc, 1) bytes (the K3 workspace
+ * followed by the fused-search scratch; heads are processed in passes as in
+ * adaspa_dense_attn_lse_search).  Argument errors as adaspa_dense_attn_lse_search and
+ * adaspa_select_blocks; nothing is launched on an error.
+ */
+adaspa_status adaspa_search_select(const adaspa_attn_desc* desc, const void* q, const void* k, const void* v,
+                                   void* o, float* lse, float* block_mass, const double* recall, uint32_t flags,
+                                   int32_t* row_ptr, int32_t* col_idx, int64_t col_capacity, int32_t* row_order,
+                                   float* head_recall, int64_t* head_nnz, void* workspace,
+                                   size_t workspace_bytes, adaspa_stream_t stream);
+
+/* Workspace bytes of adaspa_search_select for passes of `heads_per_pass` heads
+ * (<= 0 or > H: all heads in one pass). */
+size_t adaspa_search_select_workspace_bytes(const adaspa_attn_desc* desc, int32_t heads_per_pass);
 
 /*
  * K2 -- LSE-cached online search (Alg. 2; Alg. 1 second

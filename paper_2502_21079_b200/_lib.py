@@ -52,6 +52,10 @@ SYMBOLS = {
     "adaspa_lse_cached_search": (ctypes.c_int, [_D, _P, _P, _P, _P, _P]),
     "adaspa_dense_attn_lse_search": (ctypes.c_int, [_D, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
     "adaspa_fused_search_workspace_bytes": (ctypes.c_size_t, [_D, ctypes.c_int32]),
+    "adaspa_search_select": (ctypes.c_int, [_D, _P, _P, _P, _P, _P, _P, ctypes.POINTER(ctypes.c_double),
+                                             ctypes.c_uint32, _P, _P, ctypes.c_int64, _P, _P, _P, _P,
+                                             ctypes.c_size_t, _P]),
+    "adaspa_search_select_workspace_bytes": (ctypes.c_size_t, [_D, ctypes.c_int32]),
     "adaspa_select_workspace_bytes": (ctypes.c_size_t, [_D]),
     "adaspa_select_blocks": (ctypes.c_int, [_D, _P, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_uint32,
                                              ctypes.c_double, _P, _P, ctypes.c_int64, _P, _P, _P, _P,
@@ -236,6 +240,53 @@ def select_blocks(block_mass, *, heads_desc, mode, target, flags=FLAG_TEXT_SINK,
                                      _ptr(out.row_order), _ptr(out.head_recall), _ptr(out.head_nnz), _ptr(ws),
                                      wsb, _stream(stream)), "adaspa_select_blocks")
     return out
+
+
+def search_select_workspace_bytes(desc, heads_per_pass=0):
+    return int(_lib.adaspa_search_select_workspace_bytes(ctypes.byref(desc), int(heads_per_pass)))
+
+
+def search_select(q, k, v, *, block_size, n_text, target, text_first=False, softmax_scale=0.0,
+                  flags=FLAG_TEXT_SINK, o=None, lse=None, block_mass=None, want_block_mass=True, out=None,
+                  want_row_order=True, workspace=None, heads_per_pass=0, stream=None):
+    """K1 + K2 + K3 fused: the whole RECALL-mode search step t_w (adaspa_search_select).  target: per-head
+    recall r_h.  block_mass is written only if given or want_block_mass (required when nb > 2048).
+    Returns (o, lse, block_mass or None, Csr)."""
+    desc = make_desc(q, block_size, n_text, text_first, softmax_scale)
+    if o is None:
+        o = torch.empty_like(q)
+    _same_layout(desc, q, k, v, o)
+    nb = num_blocks(desc)
+    B, H = desc.batch, desc.heads
+    dev = q.device
+    if lse is None:
+        lse = torch.empty(B, H, desc.seq_len, dtype=torch.float32, device=dev)
+    _check_f32(lse, (B, H, desc.seq_len), "lse")
+    if block_mass is None and (want_block_mass or nb > 2048):
+        block_mass = torch.empty(B, H, nb, nb, dtype=torch.float32, device=dev)
+    if block_mass is not None:
+        _check_f32(block_mass, (B, H, nb, nb), "block_mass")
+    tgt = [float(x) for x in target]
+    if len(tgt) != H:
+        raise ValueError(f"need {H} per-head targets, got {len(tgt)}")
+    tarr = (ctypes.c_double * H)(*tgt)
+    rows = B * H * nb
+    if out is None:
+        out = Csr(torch.empty(rows + 1, dtype=torch.int32, device=dev),
+                  torch.empty(rows * nb, dtype=torch.int32, device=dev),
+                  torch.empty(rows, dtype=torch.int32, device=dev) if want_row_order else None,
+                  torch.empty(B, H, dtype=torch.float32, device=dev),
+                  torch.empty(B, H, dtype=torch.int64, device=dev))
+    if workspace is None:
+        workspace = _scratch(search_select_workspace_bytes(desc, heads_per_pass), dev, stream)
+    if workspace.dtype != torch.uint8 or not workspace.is_cuda:
+        raise ValueError("workspace must be a uint8 CUDA tensor")
+    _check(_lib.adaspa_search_select(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
+                                     _ptr(block_mass), tarr, int(flags), _ptr(out.row_ptr), _ptr(out.col_idx),
+                                     out.col_idx.numel(), _ptr(out.row_order), _ptr(out.head_recall),
+                                     _ptr(out.head_nnz), _ptr(workspace), workspace.numel(), _stream(stream)),
+           "adaspa_search_select")
+    return o, lse, block_mass, out
 
 
 def sparse_workspace_bytes(desc):

@@ -231,33 +231,27 @@ size_t adaspa_fused_search_workspace_bytes(const adaspa_attn_desc* desc, int32_t
   return fused_head_bytes(desc) * static_cast<size_t>(desc->batch) * hp;
 }
 
-adaspa_status adaspa_dense_attn_lse_search(const adaspa_attn_desc* desc, const void* q, const void* k, const void* v,
-                                           void* o, float* lse, float* block_mass, void* workspace,
-                                           size_t workspace_bytes, adaspa_stream_t stream) {
+namespace {
+
+// The passes of the fused search step over `ws` (>= one head of every batch element): per pass of hc
+// heads, the dense pass with block LSEs, then the block-mass reduction (with the RECALL selection
+// epilogue when sel != null and nb allows it).  Arguments validated by the caller.
+adaspa_status fused_search_passes(const adaspa_attn_desc* desc, const void* q, const void* k, const void* v,
+                                  void* o, float* lse, float* block_mass, const SelectRowsParams* sel, void* ws,
+                                  size_t ws_bytes, cudaStream_t st) {
   adaspa_status s;
-  if ((s = check_desc(desc)) != ADASPA_OK) return s;
-  if ((s = check_ptr16(q, "q")) || (s = check_ptr16(k, "k")) || (s = check_ptr16(v, "v")) ||
-      (s = check_ptr16(o, "o")))
-    return s;
-  if (!block_mass) return fail(ADASPA_ERR_INVALID_ARG, "block_mass must not be NULL");
-  if (reinterpret_cast<uintptr_t>(block_mass) % 4 || reinterpret_cast<uintptr_t>(lse) % 4)
-    return fail(ADASPA_ERR_INVALID_ARG, "lse / block_mass misaligned");
   const size_t per_head = fused_head_bytes(desc) * static_cast<size_t>(desc->batch);
-  if (!workspace || workspace_bytes < per_head)
-    return fail(ADASPA_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes (one head of every batch element)",
-                workspace_bytes, per_head);
-  const int hc = static_cast<int>(workspace_bytes / per_head < (size_t)desc->heads ? workspace_bytes / per_head
-                                                                                   : (size_t)desc->heads);
+  const int hc = static_cast<int>(ws_bytes / per_head < (size_t)desc->heads ? ws_bytes / per_head
+                                                                              : (size_t)desc->heads);
   CUtensorMap tq, tk, tv;
   const int rows_kv = desc->block_size == 64 ? 64 : 128;
   if ((s = make_map(&tq, q, desc, "q", 128)) || (s = make_map(&tk, k, desc, "k", rows_kv)) ||
       (s = make_map(&tv, v, desc, "v", rows_kv)))
     return s;
   const BlockGrid g = make_grid(desc);
-  cudaStream_t st = (cudaStream_t)stream;
   for (int h0 = 0; h0 < desc->heads; h0 += hc) {
     const int nh = desc->heads - h0 < hc ? desc->heads - h0 : hc;
-    float* blse = static_cast<float*>(workspace);
+    float* blse = static_cast<float*>(ws);
     float* lrel = blse + static_cast<size_t>(desc->batch) * nh * g.nb * desc->seq_len;
     AttnParams p{};
     p.B = desc->batch;
@@ -277,7 +271,7 @@ adaspa_status adaspa_dense_attn_lse_search(const adaspa_attn_desc* desc, const v
     p.blse = blse;
     p.lrel = lrel;
     cudaError_t e = launch_attn(tq, tk, tv, p, desc->head_dim, desc->block_size == 64, kModeBlse, num_sms(), st);
-    if (e != cudaSuccess) return cuda_fail(e, "dense_attn_lse_search launch (dense pass)");
+    if (e != cudaSuccess) return cuda_fail(e, "fused search launch (dense pass)");
     BlockMassParams m{};
     m.B = desc->batch;
     m.H = desc->heads;
@@ -288,9 +282,32 @@ adaspa_status adaspa_dense_attn_lse_search(const adaspa_attn_desc* desc, const v
     m.blse = blse;
     m.lrel = lrel;
     m.mass = block_mass;
-    if ((e = launch_block_mass(m, st)) != cudaSuccess) return cuda_fail(e, "dense_attn_lse_search launch (block mass)");
+    m.select = sel != nullptr && block_mass_select_kpl(g.nb) > 0;
+    if (m.select) m.sel = *sel;
+    if ((e = launch_block_mass(m, st)) != cudaSuccess) return cuda_fail(e, "fused search launch (block mass)");
   }
   return ADASPA_OK;
+}
+
+}  // namespace
+
+adaspa_status adaspa_dense_attn_lse_search(const adaspa_attn_desc* desc, const void* q, const void* k, const void* v,
+                                           void* o, float* lse, float* block_mass, void* workspace,
+                                           size_t workspace_bytes, adaspa_stream_t stream) {
+  adaspa_status s;
+  if ((s = check_desc(desc)) != ADASPA_OK) return s;
+  if ((s = check_ptr16(q, "q")) || (s = check_ptr16(k, "k")) || (s = check_ptr16(v, "v")) ||
+      (s = check_ptr16(o, "o")))
+    return s;
+  if (!block_mass) return fail(ADASPA_ERR_INVALID_ARG, "block_mass must not be NULL");
+  if (reinterpret_cast<uintptr_t>(block_mass) % 4 || reinterpret_cast<uintptr_t>(lse) % 4)
+    return fail(ADASPA_ERR_INVALID_ARG, "lse / block_mass misaligned");
+  const size_t per_head = fused_head_bytes(desc) * static_cast<size_t>(desc->batch);
+  if (!workspace || workspace_bytes < per_head)
+    return fail(ADASPA_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes (one head of every batch element)",
+                workspace_bytes, per_head);
+  return fused_search_passes(desc, q, k, v, o, lse, block_mass, nullptr, workspace, workspace_bytes,
+                             (cudaStream_t)stream);
 }
 
 adaspa_status adaspa_lse_cached_search(const adaspa_attn_desc* desc, const void* q, const void* k,
@@ -326,15 +343,14 @@ size_t adaspa_select_workspace_bytes(const adaspa_attn_desc* desc) {
   return select_ws_layout(desc).bytes;
 }
 
-adaspa_status adaspa_select_blocks(const adaspa_attn_desc* desc, const float* block_mass, adaspa_select_mode mode,
-                                   const double* target, uint32_t flags, double tier_tau, int32_t* row_ptr,
-                                   int32_t* col_idx, int64_t col_capacity, int32_t* row_order, float* head_recall,
-                                   int64_t* head_nnz, void* workspace, size_t workspace_bytes,
-                                   adaspa_stream_t stream) {
-  adaspa_status s;
-  if ((s = check_desc(desc)) != ADASPA_OK) return s;
-  if (!block_mass || !row_ptr || !col_idx || !target)
-    return fail(ADASPA_ERR_INVALID_ARG, "block_mass, target, row_ptr and col_idx must not be NULL");
+namespace {
+
+// Validation of the selection arguments shared by adaspa_select_blocks and adaspa_search_select.
+adaspa_status check_select(const adaspa_attn_desc* desc, adaspa_select_mode mode, const double* target,
+                           uint32_t flags, double tier_tau, const int32_t* row_ptr, const int32_t* col_idx,
+                           int64_t col_capacity) {
+  if (!row_ptr || !col_idx || !target)
+    return fail(ADASPA_ERR_INVALID_ARG, "target, row_ptr and col_idx must not be NULL");
   if (mode != ADASPA_SELECT_RECALL && mode != ADASPA_SELECT_SPARSITY)
     return fail(ADASPA_ERR_INVALID_ARG, "unknown selection mode %d", (int)mode);
   if (flags & ~3u) return fail(ADASPA_ERR_INVALID_ARG, "unknown flag bits 0x%x", flags);
@@ -348,7 +364,6 @@ adaspa_status adaspa_select_blocks(const adaspa_attn_desc* desc, const float* bl
     return fail(ADASPA_ERR_INVALID_ARG, "col_capacity %lld < B*H*nb*nb = %lld", (long long)col_capacity,
                 (long long)need_cap);
   const bool tiers = (flags & ADASPA_FLAG_HEAD_TIERS) != 0;
-  const bool sink = (flags & ADASPA_FLAG_TEXT_SINK) != 0;
   if (tiers && mode != ADASPA_SELECT_SPARSITY)
     return fail(ADASPA_ERR_INVALID_ARG, "ADASPA_FLAG_HEAD_TIERS applies to SPARSITY mode only");
   for (int h = 0; h < desc->heads; ++h) {
@@ -360,17 +375,22 @@ adaspa_status adaspa_select_blocks(const adaspa_attn_desc* desc, const float* bl
       return fail(ADASPA_ERR_INVALID_ARG, "head tiers need sparsity >= 1/3 (target[%d] = %g)", h, t);
   }
   if (tiers && !(tier_tau == tier_tau)) return fail(ADASPA_ERR_INVALID_ARG, "tier_tau is NaN");
-  const SelectWs w = select_ws_layout(desc);
-  if (!workspace || workspace_bytes < w.bytes)
-    return fail(ADASPA_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", workspace_bytes, w.bytes);
-  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  return ADASPA_OK;
+}
 
+// Launch parameters of the selection over a K3 workspace `ws` (select_ws_layout).
+void build_select(const adaspa_attn_desc* desc, const float* block_mass, adaspa_select_mode mode,
+                  const double* target, uint32_t flags, double tier_tau, int32_t* row_ptr, int32_t* col_idx,
+                  int32_t* row_order, float* head_recall, int64_t* head_nnz, uint8_t* ws, SelectLaunch& L) {
+  const BlockGrid g = make_grid(desc);
+  const SelectWs w = select_ws_layout(desc);
+  const int64_t rows = (int64_t)desc->batch * desc->heads * g.nb;
+  const bool sink = (flags & ADASPA_FLAG_TEXT_SINK) != 0;
   const int n_text_blocks = desc->text_first ? g.nb_first : g.nb - g.nb_first;
   const int ncand = sink ? g.nb - n_text_blocks : g.nb;
-
-  SelectLaunch L{};
+  L = SelectLaunch{};
   L.batch = desc->batch;
-  L.tiers = tiers;
+  L.tiers = (flags & ADASPA_FLAG_HEAD_TIERS) != 0;
   SelectRowsParams& rp = L.rows;
   rp.mass = block_mass;
   rp.rows = static_cast<int>(rows);
@@ -425,8 +445,72 @@ adaspa_status adaspa_select_blocks(const adaspa_attn_desc* desc, const float* bl
   wp.row_ptr = row_ptr;
   wp.row_order = row_order;
   wp.col_idx = col_idx;
+}
+
+}  // namespace
+
+adaspa_status adaspa_select_blocks(const adaspa_attn_desc* desc, const float* block_mass, adaspa_select_mode mode,
+                                   const double* target, uint32_t flags, double tier_tau, int32_t* row_ptr,
+                                   int32_t* col_idx, int64_t col_capacity, int32_t* row_order, float* head_recall,
+                                   int64_t* head_nnz, void* workspace, size_t workspace_bytes,
+                                   adaspa_stream_t stream) {
+  adaspa_status s;
+  if ((s = check_desc(desc)) != ADASPA_OK) return s;
+  if (!block_mass) return fail(ADASPA_ERR_INVALID_ARG, "block_mass must not be NULL");
+  if ((s = check_select(desc, mode, target, flags, tier_tau, row_ptr, col_idx, col_capacity)) != ADASPA_OK) return s;
+  const SelectWs w = select_ws_layout(desc);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ADASPA_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", workspace_bytes, w.bytes);
+  SelectLaunch L;
+  build_select(desc, block_mass, mode, target, flags, tier_tau, row_ptr, col_idx, row_order, head_recall, head_nnz,
+               static_cast<uint8_t*>(workspace), L);
   cudaError_t e = launch_select(L, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "select_blocks launch");
+  return ADASPA_OK;
+}
+
+size_t adaspa_search_select_workspace_bytes(const adaspa_attn_desc* desc, int32_t heads_per_pass) {
+  if (check_desc(desc) != ADASPA_OK) return 0;
+  const int hp = (heads_per_pass <= 0 || heads_per_pass > desc->heads) ? desc->heads : heads_per_pass;
+  return align256(select_ws_layout(desc).bytes) + fused_head_bytes(desc) * static_cast<size_t>(desc->batch) * hp;
+}
+
+adaspa_status adaspa_search_select(const adaspa_attn_desc* desc, const void* q, const void* k, const void* v, void* o,
+                                   float* lse, float* block_mass, const double* recall, uint32_t flags,
+                                   int32_t* row_ptr, int32_t* col_idx, int64_t col_capacity, int32_t* row_order,
+                                   float* head_recall, int64_t* head_nnz, void* workspace, size_t workspace_bytes,
+                                   adaspa_stream_t stream) {
+  adaspa_status s;
+  if ((s = check_desc(desc)) != ADASPA_OK) return s;
+  if ((s = check_ptr16(q, "q")) || (s = check_ptr16(k, "k")) || (s = check_ptr16(v, "v")) ||
+      (s = check_ptr16(o, "o")))
+    return s;
+  if (flags & ADASPA_FLAG_HEAD_TIERS)
+    return fail(ADASPA_ERR_INVALID_ARG, "adaspa_search_select is RECALL mode: ADASPA_FLAG_HEAD_TIERS not allowed");
+  if ((s = check_select(desc, ADASPA_SELECT_RECALL, recall, flags, 0.0, row_ptr, col_idx, col_capacity)) != ADASPA_OK)
+    return s;
+  const BlockGrid g = make_grid(desc);
+  const bool fused_select = block_mass_select_kpl(g.nb) > 0;
+  if (!block_mass && !fused_select)
+    return fail(ADASPA_ERR_INVALID_ARG, "block_mass may be NULL only for nb <= 2048 (nb = %d)", g.nb);
+  if (reinterpret_cast<uintptr_t>(block_mass) % 4 || reinterpret_cast<uintptr_t>(lse) % 4)
+    return fail(ADASPA_ERR_INVALID_ARG, "lse / block_mass misaligned");
+  const size_t sel_bytes = align256(select_ws_layout(desc).bytes);
+  const size_t per_head = fused_head_bytes(desc) * static_cast<size_t>(desc->batch);
+  if (!workspace || workspace_bytes < sel_bytes + per_head)
+    return fail(ADASPA_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes (selection + one head of every batch element)",
+                workspace_bytes, sel_bytes + per_head);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  SelectLaunch L;
+  build_select(desc, block_mass, ADASPA_SELECT_RECALL, recall, flags, 0.0, row_ptr, col_idx, row_order, head_recall,
+               head_nnz, ws, L);
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((s = fused_search_passes(desc, q, k, v, o, lse, block_mass, &L.rows, ws + sel_bytes, workspace_bytes - sel_bytes,
+                               st)) != ADASPA_OK)
+    return s;
+  cudaError_t e;
+  if (!fused_select && (e = launch_select_rows(L.rows, st)) != cudaSuccess) return cuda_fail(e, "search_select launch (rows)");
+  if ((e = launch_select_final(L, st)) != cudaSuccess) return cuda_fail(e, "search_select launch (CSR)");
   return ADASPA_OK;
 }
 

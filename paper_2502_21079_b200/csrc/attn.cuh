@@ -3,6 +3,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "select.cuh"
 
 namespace adaspa {
 
@@ -50,7 +51,12 @@ struct BlockMassParams {
   BlockGrid grid;
   const float* blse;
   const float* lrel;
-  float* mass;               // [B, H, nb, nb]
+  float* mass;               // [B, H, nb, nb], or null (not written: the selection epilogue consumes the row)
+  // RECALL selection epilogue (f1): with select != 0, warp 0 of each CTA selects its q-block row from the
+  // shared-memory mass row (select_row.cuh, the same routine as K3's select_rows_kernel) into the K3
+  // workspace arrays of `sel` (row = (b*H + h)*nb + qb); `sel.mass` is unused.
+  int select;
+  SelectRowsParams sel;
 };
 
 struct SparsePrepParams {
@@ -81,6 +87,8 @@ cudaError_t launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUte
                         const AttnParams& p, int head_dim, bool two, int mode, int num_sms,
                         cudaStream_t st);
 cudaError_t launch_block_mass(const BlockMassParams& p, cudaStream_t st);
+// rows per lane of the fused selection epilogue: 0 (nb too large: run K3's select_rows after the passes)
+int block_mass_select_kpl(int nb);
 cudaError_t launch_sparse_prep(const SparsePrepParams& p, cudaStream_t st);
 cudaError_t launch_search(const CUtensorMap& tq, const CUtensorMap& tk, const SearchParams& p, int head_dim,
                           bool two, int num_sms, cudaStream_t st);

@@ -12,6 +12,7 @@
 // and does one exponential per (row, kv block).
 #include "attn.cuh"
 #include "common.cuh"
+#include "select_row.cuh"
 
 namespace adaspa {
 
@@ -22,8 +23,13 @@ constexpr int kWarps = 8;
 // One CTA per (b, h, q-block): warp w takes kv blocks w, w+8, ...; lane l holds rows l + 32r of the
 // q-block (coalesced 128-byte loads along the token axis of blse[b,h,kb,:]); the q-block's mass row
 // is staged in shared memory and written contiguously.
-template <int R>
-__global__ void __launch_bounds__(kWarps * 32) block_mass_kernel(BlockMassParams p) {
+// 5 CTAs per SM (48 registers) keep enough loads in flight for HBM; the selection epilogue spills a
+// few words at that size (one warp, once per CTA).
+// KPL > 0: the RECALL selection epilogue of the fused search (f1) -- warp 0 selects the row from the
+// shared-memory masses with K3's routine (select_row.cuh), so the mass row never makes a round trip
+// through HBM for the selection; KPL = ceil(nb/32) rounded up to an instantiated size.
+template <int R, int KPL>
+__global__ void __launch_bounds__(kWarps * 32, 5) block_mass_kernel(BlockMassParams p) {
   extern __shared__ float mrow[];
   const int nb = p.grid.nb;
   const int qb = blockIdx.x % nb;
@@ -73,28 +79,64 @@ __global__ void __launch_bounds__(kWarps * 32) block_mass_kernel(BlockMassParams
     if ((lane & 7) == 0 && kb < nb) mrow[kb] = c;
   }
   __syncthreads();
-  float* out = p.mass + ((static_cast<int64_t>(b) * p.H + h) * nb + qb) * nb;
-  for (int j = threadIdx.x; j < nb; j += kWarps * 32) out[j] = mrow[j];
+  const int64_t row = (static_cast<int64_t>(b) * p.H + h) * nb + qb;
+  if (p.mass) {
+    float* out = p.mass + row * nb;
+    for (int j = threadIdx.x; j < nb; j += kWarps * 32) out[j] = mrow[j];
+  }
+  if constexpr (KPL > 0) {
+    __syncthreads();  // the row is rewritten in place below (non-candidates -> 0, padding to 32*KPL)
+    if (warp == 0) {
+      selrow::SmemRow<KPL> mr(mrow);
+      selrow::select_row<KPL>(p.sel, static_cast<int>(row), lane, mr, [&](int j) { return mrow[j]; });
+    }
+  }
+}
+
+template <int R, int KPL>
+cudaError_t launch_bm(const BlockMassParams& p, int64_t ctas, size_t smem, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(block_mass_kernel<R, KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+    return e;
+  block_mass_kernel<R, KPL><<<static_cast<unsigned>(ctas), kWarps * 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int R>
+cudaError_t launch_bm_r(const BlockMassParams& p, int64_t ctas, size_t smem, cudaStream_t st) {
+  switch (p.select ? block_mass_select_kpl(p.grid.nb) : 0) {
+    case 4: return launch_bm<R, 4>(p, ctas, smem, st);
+    case 8: return launch_bm<R, 8>(p, ctas, smem, st);
+    case 16: return launch_bm<R, 16>(p, ctas, smem, st);
+    case 24: return launch_bm<R, 24>(p, ctas, smem, st);
+    case 28: return launch_bm<R, 28>(p, ctas, smem, st);
+    case 32: return launch_bm<R, 32>(p, ctas, smem, st);
+    case 64: return launch_bm<R, 64>(p, ctas, smem, st);
+    default: return launch_bm<R, 0>(p, ctas, smem, st);
+  }
 }
 
 }  // namespace
+
+int block_mass_select_kpl(int nb) {
+  const int k = (nb + 31) / 32;
+  if (k <= 4) return 4;
+  if (k <= 8) return 8;
+  if (k <= 16) return 16;
+  if (k <= 24) return 24;
+  if (k <= 28) return 28;
+  if (k <= 32) return 32;
+  if (k <= 64) return 64;
+  return 0;  // nb > 2048: the selection runs as K3's select_rows kernel after the passes
+}
 
 cudaError_t launch_block_mass(const BlockMassParams& p, cudaStream_t st) {
   const int64_t ctas = static_cast<int64_t>(p.B) * p.nh * p.grid.nb;
   if (ctas <= 0) return cudaSuccess;
   if (ctas > 0x7fffffffLL) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(float) * p.grid.nb;
-  cudaError_t e;
-  if (p.grid.bs == 64) {
-    if ((e = cudaFuncSetAttribute(block_mass_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
-      return e;
-    block_mass_kernel<2><<<static_cast<unsigned>(ctas), kWarps * 32, smem, st>>>(p);
-  } else {
-    if ((e = cudaFuncSetAttribute(block_mass_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
-      return e;
-    block_mass_kernel<4><<<static_cast<unsigned>(ctas), kWarps * 32, smem, st>>>(p);
-  }
-  return cudaGetLastError();
+  const int kpl = p.select ? block_mass_select_kpl(p.grid.nb) : 0;
+  const size_t smem = sizeof(float) * (kpl > 0 ? 32 * kpl : p.grid.nb);
+  return p.grid.bs == 64 ? launch_bm_r<2>(p, ctas, smem, st) : launch_bm_r<4>(p, ctas, smem, st);
 }
 
 }  // namespace adaspa

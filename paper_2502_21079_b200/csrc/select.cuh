@@ -72,6 +72,9 @@ struct SelectLaunch {
 };
 
 cudaError_t launch_select(const SelectLaunch& L, cudaStream_t st);
+// the two halves of launch_select (no tiers): per-row selection, then CSR assembly from its arrays
+cudaError_t launch_select_rows(const SelectRowsParams& p, cudaStream_t st);
+cudaError_t launch_select_final(const SelectLaunch& L, cudaStream_t st);
 
 __host__ __device__ int k_from_sparsity(double s, int n);
 constexpr int kMaxSelectBlocks = 6144;  // one warp holds a row: 192 masses per lane at most

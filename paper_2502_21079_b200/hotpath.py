@@ -4,9 +4,11 @@
     every later step:          K4 block-sparse forward on the cached CSR
     later key steps (Alg. 2):  K2 block mass with the cached LSE  ->  K3
 
-`search(fused=True)` runs Alg. 1 as ONE dense pass that also emits per-(row, kv block)
-log-sum-exps plus an HBM-bound block-mass reduction (adaspa_dense_attn_lse_search);
-`search(fused=False)` runs it as K1 then K2 with the fresh LSE.  Buffers are allocated once;
+`search(fused=True)` runs the whole search step t_w in ONE C-ABI call (adaspa_search_select): one
+dense pass that also emits per-(row, kv block) log-sum-exps, then an HBM-bound block-mass reduction
+whose CTAs select their q-block row (RECALL) before the CSR is assembled; `search(fused="mass")` runs
+the fused dense pass + block masses (adaspa_dense_attn_lse_search) then K3; `search(fused=False)`
+runs K1, K2 with the fresh LSE, K3.  Buffers are allocated once;
 `run()` accepts device tensors or (pinned) host tensors, in which case it stages them to the
 device on the same stream; `run_sparse_host()` is a sparse step end to end from host memory.
 Everything runs through the C ABI; nothing here computes.
@@ -48,7 +50,7 @@ class HotPath:
         self.csr = L.Csr(e(rows + 1, dt=torch.int32), e(rows * self.nb, dt=torch.int32), e(rows, dt=torch.int32),
                          e(batch, heads, dt=torch.float32), e(batch, heads, dt=torch.int64))
         self.ws = e(max(L.sparse_workspace_bytes(self.desc), 1), dt=torch.uint8)
-        self.fws = None     # fused-search scratch (4*(nb+1)*N bytes per head), allocated on first use
+        self.fws = None     # fused-search scratch (K3 workspace + 4*(nb+1)*N bytes per head), on first use
         self.mass2 = None   # block masses of a later key step (K2 with the cached LSE)
 
     def _stage(self, q, k, v):
@@ -65,15 +67,27 @@ class HotPath:
 
     def search(self, q, k, v, events=None, fused=True):
         """The search step t_w (Alg. 1) into self.o_dense, self.lse (the LSE cache), self.mass and
-        self.csr.  fused: K1+K2 in one dense pass (adaspa_dense_attn_lse_search), else K1 then K2.
-        events: optional list of 4 CUDA events recorded around K1, K2, K3 (fused: the whole fused
-        call between events 0 and 1, nothing between 1 and 2)."""
+        self.csr.  fused=True: one call, adaspa_search_select (RECALL without tiers; otherwise as "mass");
+        fused="mass": adaspa_dense_attn_lse_search then K3; fused=False: K1, K2, K3.  events: optional
+        list of 4 CUDA events recorded around K1, K2, K3 (a fused call lies between events 0 and 1)."""
         q, k, v = self._stage(q, k, v)
         rec = (lambda i: events[i].record()) if events else (lambda i: None)  # noqa: E731
+        if fused is True and not self.select_fusable():
+            fused = "mass"
         rec(0)
+        if fused is True:
+            if self.fws is None:
+                self.fws = torch.empty(L.search_select_workspace_bytes(self.desc, 0), dtype=torch.uint8,
+                                       device=self.device)
+            L.search_select(q, k, v, target=self.targets, flags=self.flags, o=self.o_dense, lse=self.lse,
+                            block_mass=self.mass, out=self.csr, workspace=self.fws, **self.kw)
+            rec(1)
+            rec(2)
+            rec(3)
+            return self.csr
         if fused:
             if self.fws is None:
-                self.fws = torch.empty(L.fused_search_workspace_bytes(self.desc, 0), dtype=torch.uint8,
+                self.fws = torch.empty(L.search_select_workspace_bytes(self.desc, 0), dtype=torch.uint8,
                                        device=self.device)
             L.dense_attn_lse_search(q, k, v, o=self.o_dense, lse=self.lse, block_mass=self.mass,
                                     workspace=self.fws, **self.kw)
@@ -83,9 +97,18 @@ class HotPath:
             rec(1)
             L.lse_cached_search(q, k, self.lse, block_mass=self.mass, **self.kw)
         rec(2)
-        L.select_blocks(self.mass, heads_desc=self.desc, mode=self.mode, target=self.targets, flags=self.flags,
-                        tier_tau=self.tier_tau, out=self.csr)
+        self.select(self.mass)
         rec(3)
+        return self.csr
+
+    def select_fusable(self):
+        """The selection epilogue of adaspa_search_select covers RECALL mode without head tiers."""
+        return self.mode == L.SELECT_RECALL and not (self.flags & L.FLAG_HEAD_TIERS)
+
+    def select(self, mass):
+        """K3 on the given block masses into self.csr (a later key step selects on K2's masses)."""
+        L.select_blocks(mass, heads_desc=self.desc, mode=self.mode, target=self.targets, flags=self.flags,
+                        tier_tau=self.tier_tau, out=self.csr)
         return self.csr
 
     def dense(self, q, k, v, o=None, lse=None):
@@ -120,9 +143,12 @@ class HotPath:
             events[4].record()
         return self.o_sparse
 
-    # launches of our kernels per run(): fused search 2 (dense pass + block mass; K1 + K2 unfused), K3 4
-    # (rows, head, scan, write; +2 with tiers), K4 3 (stream + order + attention)
+    # launches of our kernels per run(): search step 5 (dense pass, block mass + selection epilogue, head,
+    # scan, write; RECALL) or 6 (dense pass, block mass, K3's rows, head, scan, write; +2 with tiers), K4 3
+    # (stream + order + attention)
     def kernels_per_run(self):
+        if self.select_fusable() and L.num_blocks(self.desc) <= 2048:
+            return 8
         return 9 + (2 if self.flags & L.FLAG_HEAD_TIERS else 0)
 
     def run_sparse_host(self, q_host, k_host, v_host, o_host, groups=24):

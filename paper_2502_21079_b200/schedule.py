@@ -2,8 +2,10 @@
 
 PAPER.md:397-405 (fig:overview caption): warm-up steps run full attention; the first key step
 t_key^1 = t_w runs the Fused Online Search (Alg. 1: dense attention that also emits the LSE, then
-the block mass with that fresh LSE, PAPER.md:459-497 -- here one dense pass that also emits the
-per-(row, kv block) log-sum-exps, adaspa_dense_attn_lse_search, unless fused_search=False); every later key step runs the LSE-Cached
+the block mass with that fresh LSE, PAPER.md:459-497 -- here ONE C-ABI call, adaspa_search_select:
+one dense pass that also emits the per-(row, kv block) log-sum-exps, the block masses whose CTAs
+select their q-block row (RECALL), the CSR; SPARSITY / tiers: adaspa_dense_attn_lse_search then K3;
+fused_search=False: K1, K2, K3); every later key step runs the LSE-Cached
 Online Search (Alg. 2) with the LSE cached at t_w; all other steps after t_w run
 the head-adaptive block-sparse attention with the cached index lists.
 Defaults: T_s = {10, 30}, 10 warm-up steps, 50 steps.
@@ -115,14 +117,19 @@ class AdaSpaSchedule:
             L.dense_attn_lse(q, k, v, o=o, want_lse=False, **self.kw)
         elif mode == FULL_SEARCH:
             if self.fused_search:                                    # Alg. 1 in one dense pass
-                need = L.fused_search_workspace_bytes(desc, self.fused_heads_per_pass)
+                need = L.search_select_workspace_bytes(desc, self.fused_heads_per_pass)
                 if self._fws is None or self._fws.numel() < need:
                     self._fws = torch.empty(need, dtype=torch.uint8, device=q.device)
-                L.dense_attn_lse_search(q, k, v, o=o, lse=c.lse, block_mass=c.mass, workspace=self._fws,
-                                        **self.kw)                   # λ from t_w becomes the cache (R19)
+                if self.mode == L.SELECT_RECALL and not (self.flags & L.FLAG_HEAD_TIERS):
+                    # the whole search step, selection epilogue included; λ from t_w becomes the cache (R19)
+                    L.search_select(q, k, v, target=self._targets(desc.heads), flags=self.flags, o=o, lse=c.lse,
+                                    block_mass=c.mass, out=c.csr, workspace=self._fws, **self.kw)
+                else:
+                    L.dense_attn_lse_search(q, k, v, o=o, lse=c.lse, block_mass=c.mass, workspace=self._fws,
+                                            **self.kw)               # λ from t_w becomes the cache (R19)
+                    L.select_blocks(c.mass, heads_desc=desc, mode=self.mode, target=self._targets(desc.heads),
+                                    flags=self.flags, tier_tau=self.tier_tau, out=c.csr)
                 c.have_lse = True
-                L.select_blocks(c.mass, heads_desc=desc, mode=self.mode, target=self._targets(desc.heads),
-                                flags=self.flags, tier_tau=self.tier_tau, out=c.csr)
                 c.have_mask = True
             else:
                 L.dense_attn_lse(q, k, v, o=o, lse=c.lse, **self.kw)   # λ from t_w becomes the cache (R19)

@@ -26,7 +26,7 @@ def lib():
 
 def test_exports_every_header_symbol(lib):
     names = _header_functions()
-    assert len(names) == 12, names
+    assert len(names) == 14, names
     for n in names:
         assert hasattr(lib._lib, n), n
         assert n in lib.SYMBOLS, n
@@ -129,3 +129,48 @@ def test_fused_search_workspace_and_errors(lib):
     assert st == lib.ERR_INVALID_ARG and b"block_mass" in L.adaspa_last_error()
     st = L.adaspa_dense_attn_lse_search(ctypes.byref(d), nul, fake, fake, fake, fake, fake, fake, per, nul)
     assert st == lib.ERR_INVALID_ARG
+
+
+def test_search_select_workspace_and_errors(lib):
+    """adaspa_search_select (the whole RECALL search step t_w): workspace = the K3 workspace (256-B
+    aligned) + the fused-search scratch per head pass; argument errors rejected before any launch."""
+    L = lib._lib
+    d = _desc(lib)
+    nb = lib.num_blocks(d)
+    per = 4 * (nb + 1) * d.seq_len * d.batch
+    sel = int(L.adaspa_select_workspace_bytes(ctypes.byref(d)))
+    sel = (sel + 255) // 256 * 256
+    assert lib.search_select_workspace_bytes(d, 1) == sel + per
+    assert lib.search_select_workspace_bytes(d, 0) == sel + per * d.heads
+    fake = ctypes.c_void_p(0x10000)
+    nul = ctypes.c_void_p(0)
+    H = d.heads
+    ok = (ctypes.c_double * H)(*([0.9] * H))
+    cap = d.batch * H * nb * nb
+
+    def call(q=fake, mass=fake, tgt=ok, flags=1, rp=fake, cap=cap, ws=sel + per):
+        return L.adaspa_search_select(ctypes.byref(d), q, fake, fake, fake, fake, mass, tgt, flags, rp, fake, cap,
+                                      nul, nul, nul, fake, ws, nul)
+
+    assert call(ws=sel + per - 1) == lib.ERR_WORKSPACE_TOO_SMALL
+    assert call(q=nul) == lib.ERR_INVALID_ARG
+    assert call(rp=nul) == lib.ERR_INVALID_ARG
+    assert call(cap=cap - 1) == lib.ERR_INVALID_ARG
+    assert call(flags=3) == lib.ERR_INVALID_ARG and b"TIERS" in L.adaspa_last_error()
+    bad = (ctypes.c_double * H)(*([float("nan")] * H))
+    assert call(tgt=bad) == lib.ERR_INVALID_ARG
+
+
+def test_search_select_needs_block_mass_above_2048_blocks(lib):
+    """nb > 2048: the selection runs on the written masses, so block_mass = NULL is an argument error."""
+    L = lib._lib
+    d = lib.AttnDesc(1, 1, 140000, 64, 64, 0, 0, 0.0, 140000 * 64, 140000 * 64, 64)
+    assert lib.num_blocks(d) > 2048
+    fake = ctypes.c_void_p(0x10000)
+    nul = ctypes.c_void_p(0)
+    nb = lib.num_blocks(d)
+    ws = lib.search_select_workspace_bytes(d, 0)
+    tg = (ctypes.c_double * 1)(0.9)
+    st = L.adaspa_search_select(ctypes.byref(d), fake, fake, fake, fake, fake, nul, tg, 1, fake, fake, nb * nb,
+                                nul, nul, nul, fake, ws, nul)
+    assert st == lib.ERR_INVALID_ARG and b"2048" in L.adaspa_last_error()

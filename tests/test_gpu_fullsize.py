@@ -40,7 +40,13 @@ def test_fullsize_hot_path_sampled(ada, name):
     hp = HotPath(1, lay.heads, lay.n, lay.head_dim, lay.block, lay.n_text, lay.text_first,
                  mode=ada.SELECT_RECALL, targets=0.9, flags=ada.FLAG_TEXT_SINK)
     o = hp.run(q, k, v)
+    # the search step's fused selection epilogue == K3 on the masses it wrote, whole layer, bit for bit
+    ref = ada.select_blocks(hp.mass, heads_desc=hp.desc, mode=ada.SELECT_RECALL, target=[0.9] * lay.heads,
+                            flags=ada.FLAG_TEXT_SINK)
     torch.cuda.synchronize()
+    assert torch.equal(ref.row_ptr, hp.csr.row_ptr)
+    assert torch.equal(ref.col_idx[:int(ref.row_ptr[-1])], hp.csr.col_idx[:int(ref.row_ptr[-1])])
+    assert torch.equal(ref.head_recall, hp.csr.head_recall)
     blocks = oracle.block_map(lay.n_video, lay.n_text, lay.block, lay.text_first)
     nb = len(blocks)
     assert nb == hp.nb

@@ -1,6 +1,7 @@
 """One bench step on a BASELINE config for ncu captures (diagnostic; not the bench contract):
-K1 alone, the fused search (dense BLSE pass + block mass), K3, K4, K2 with the cached LSE -- the
-kernels in that launch order (attn_fwd_kernel: dense, then BLSE, then sparse).
+K1 alone, the search step t_w in one call (dense BLSE pass, block mass + selection epilogue, CSR), K4,
+K2 with the cached LSE, K3 on its masses -- the kernels in that launch order (attn_fwd_kernel: dense,
+then BLSE, then sparse).
 
     python tools/prof_step.py [config] [runs]
 """
@@ -25,6 +26,6 @@ for _ in range(runs):
     hp.dense(q, k, v, o=o)
     hp.search(q, k, v)
     hp.sparse(q, k, v)
-    hp.cached_search(q, k)
+    hp.select(hp.cached_search(q, k))
 torch.cuda.synchronize()
 print("done", name, runs)
