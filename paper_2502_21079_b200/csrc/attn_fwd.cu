@@ -85,6 +85,12 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define ADASPA_ABLATE 0  // diagnostic builds only: 4 = no softmax (MMA / TMA pipeline alone)
 #endif
 constexpr int kExpPolyMod = ADASPA_EXP_POLY_MOD;
+#ifndef ADASPA_ARRIVE_RELAXED
+#define ADASPA_ARRIVE_RELAXED 0
+#endif
+#ifndef ADASPA_BLSE_ABL
+#define ADASPA_BLSE_ABL 0  // diagnostic builds only: 1 = no per-tile block-LSE epilogue, 2 = no store
+#endif
 
 enum : int { kNormal = 0, kEnd = 1, kAllEnd = 2 };
 
@@ -99,7 +105,6 @@ struct TileInfo {
   int has;         // END: this tile had >= 1 entry in the item (O must be stored)
   int b, h;
   int start0, len0, start1, len1;
-  int kb0, kb1;    // BLSE mode, normal tiles: kv block ids of the tile (kb1 = -1: one block per tile)
 };
 
 struct ItemInfo {
@@ -521,8 +526,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 inf.h = it.h;
                 inf.start0 = it.start0[t];
                 inf.len0 = it.len0[t];
-                inf.kb0 = mt.id0;
-                inf.kb1 = mt.id1;
               }
               tc_commit(&bars->s_full[t]);
               mbar_arrive(&bars->s_full[t]);
@@ -589,7 +592,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     float m_used[2] = {-INFINITY, -INFINITY};
     float l_sum[2] = {0.0f, 0.0f};  // this thread's share (its 32 columns) of the row sums
     float ref[2] = {0.0f, 0.0f};    // BLSE: the row's first running max (log2 units)
+    float mref = 0.0f;              // BLSE: m_used - ref of this lane's block-LSE row (qd & 1), kept with m
     int ntile = 0;
+    float* blse_row = nullptr;  // BLSE: this lane's row of the block-LSE scratch (per item)
+    bool blse_ok = false;
     int tr_k = 0;
     (void)tr_k;
     const Poly3x2 poly;
@@ -597,6 +603,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     // polynomial (rel. error 2.3e-7, ex2.approx class) instead of the degree-3 one (7.5e-5, enough
     // for P's bf16 rounding but not for a block mass to ~1e-6)
     const Poly5x2 poly5;
+    // BLSE: a tile's per-(row, kv block) sums, quad-reduced, as log-sum-exps relative to the row's ref:
+    // log2 sum_{j in kb} 2^(s_ij*scale*log2e) - ref_i = log2(t) + (m_used - ref).  Quad lane qd writes
+    // (row qd&1, block half qd>>1), rows of a warp contiguous in blse[bh][kb][.].  The transpose-reduce
+    // over the quad halves the values a lane keeps per exchange, so lane qd ends with value qd in 2
+    // shuffles (one block per tile) or 3 (KVTWO).  (Deferring this to the next tile's first P hand-off
+    // measured slower: profiles/r02k_ab_*.txt.)
+    auto blse_store = [&](float t0v, float t1v, float h0v, float h1v, int tile) {
+      const int j = qd & 1, hf = qd >> 1;
+      float tt;
+      if (KVTWO) {
+        // values: (r0,h0) (r1,h0) (r0,h1) (r1,h1); xor 2 splits the halves, xor 1 the rows
+        const float keep0 = hf ? t0v : h0v, send0 = hf ? h0v : t0v;
+        const float keep1 = hf ? t1v : h1v, send1 = hf ? h1v : t1v;
+        const float r0 = keep0 + __shfl_xor_sync(0xffffffffu, send0, 2);
+        const float r1 = keep1 + __shfl_xor_sync(0xffffffffu, send1, 2);
+        const float keep = j ? r1 : r0, send = j ? r0 : r1;
+        tt = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+      } else {
+        const float keep = j ? t1v : t0v, send = j ? t0v : t1v;
+        tt = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+        tt += __shfl_xor_sync(0xffffffffu, tt, 2);
+      }
+      // kv tiles follow the block grid, every tile of the item in order: tile n is block n (KVTWO:
+      // blocks 2n and 2n+1)
+      const int kb = KVTWO ? 2 * tile + hf : tile;
+      if (blse_ok && kb < p.grid.nb) {
+        const float Lb = __log2f(tt) + mref;  // tt = 0 (or a denormal): -inf
+        if (ADASPA_BLSE_ABL != 2 || p.N < 0) __stcs(blse_row + static_cast<int64_t>(kb) * p.N, Lb);  // streamed: K/V stay in L2
+      }
+    };
     for (;;) {
       mbar_wait(&bars->s_full[t], sph);
       sph ^= 1;
@@ -693,6 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         m_used[0] = m_used[1] = -INFINITY;
         l_sum[0] = l_sum[1] = 0.0f;
         ref[0] = ref[1] = 0.0f;
+        mref = 0.0f;
         ntile = 0;
         continue;
       }
@@ -714,6 +751,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       // (volatile) before the TMEM load, used only before the exponentials
       const int limA = *reinterpret_cast<const volatile int*>(&inf.lim[hq * 2 + 0]);
       const int limB = *reinterpret_cast<const volatile int*>(&inf.lim[hq * 2 + 1]);
+      if (BLSE && ntile == 0) {  // per item: this lane's row in blse[b,h][kb][.] and whether it stores
+        const int row = (qd & 1) ? row1 : row0;
+        const int64_t bhl = static_cast<int64_t>(inf.b) * p.nh + (inf.h - p.h0);
+        blse_row = p.blse + bhl * p.grid.nb * p.N + inf.start0 + row;
+        blse_ok = (KVTWO || (qd >> 1) == 0) && row < inf.len0;
+      }
       uint32_t s[64];
       tmem_ld_16x256b_x8(s_addr, s);
       tmem_ld_16x256b_x8(s_addr + 64, s + 32);
@@ -768,6 +811,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             rescale |= alpha[j] != 0.0f && ntile > 0;
           }
         }
+        if (BLSE) mref = (qd & 1) ? (m_used[1] - ref[1]) : (m_used[0] - ref[0]);
       };
       {
         const float lmx0 = fmaxf(mxa[0], mxb[0]) * sl2, lmx1 = fmaxf(mxa[1], mxb[1]) * sl2;
@@ -858,7 +902,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&bars->p_half[t]);
+          if (lane == 0) {
+            if (ADASPA_ARRIVE_RELAXED) mbar_arrive_relaxed(&bars->p_half[t]); else mbar_arrive(&bars->p_half[t]);
+          }
           if (BLSE && KVTWO) {  // kv block id0 ends here: keep its row sums apart from block id1's
             const float2 h0 = fadd2(acc[0], acc[2]), h1 = fadd2(acc[1], acc[3]);
             half0[0] = h0.x + h0.y;
@@ -876,37 +922,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       ADASPA_TRACE_EV(3);
-      if (lane == 0) mbar_arrive(&bars->p_full[t]);
-      if (BLSE) {
-        // Off the critical path (P is handed over): the tile's per-(row, kv block) sums, quad-reduced,
-        // as log-sum-exps relative to the row's ref: log2 sum_{j in kb} 2^(s_ij*scale*log2e) - ref_i
-        // = log2(t) + (m_used - ref).  Quad lane qd writes (row qd&1, block half qd>>1), rows of a warp
-        // contiguous in blse[bh][kb][.] (16 rows x 4 B per store instruction and block).
-        // transpose-reduce over the quad: each exchange halves the values a lane keeps, so lane qd
-        // ends with value qd (row qd&1, half qd>>1) in 2 shuffles (one block) or 3 (KVTWO), not 4 / 8
-        const int j = qd & 1, hf = qd >> 1;
-        float tt;
-        if (KVTWO) {
-          // values: (r0,h0) (r1,h0) (r0,h1) (r1,h1); xor 2 splits the halves, xor 1 the rows
-          const float keep0 = hf ? tsum[0] : half0[0], send0 = hf ? half0[0] : tsum[0];
-          const float keep1 = hf ? tsum[1] : half0[1], send1 = hf ? half0[1] : tsum[1];
-          const float r0 = keep0 + __shfl_xor_sync(0xffffffffu, send0, 2);
-          const float r1 = keep1 + __shfl_xor_sync(0xffffffffu, send1, 2);
-          const float keep = j ? r1 : r0, send = j ? r0 : r1;
-          tt = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-        } else {
-          const float keep = j ? tsum[1] : tsum[0], send = j ? tsum[0] : tsum[1];
-          tt = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-          tt += __shfl_xor_sync(0xffffffffu, tt, 2);
-        }
-        const int kb = hf ? inf.kb1 : inf.kb0;
-        const int row = j ? row1 : row0;
-        if ((KVTWO || hf == 0) && kb >= 0 && row < inf.len0) {
-          const float Lb = tt > 0x1p-100f ? __log2f(tt) + (m_used[j] - ref[j]) : -INFINITY;
-          const int64_t bhl = static_cast<int64_t>(inf.b) * p.nh + (inf.h - p.h0);
-          p.blse[(bhl * p.grid.nb + kb) * p.N + inf.start0 + row] = Lb;
-        }
+      if (lane == 0) {
+        if (ADASPA_ARRIVE_RELAXED) mbar_arrive_relaxed(&bars->p_full[t]); else mbar_arrive(&bars->p_full[t]);
       }
+      // off the critical path (P is handed over): this tile's block log-sum-exps
+      if (BLSE && ADASPA_BLSE_ABL != 1) blse_store(tsum[0], tsum[1], half0[0], half0[1], ntile);
       ++ntile;
     }
   }
