@@ -68,6 +68,18 @@ def test_dense_all_logits_far_below_zero(ada, d, n):
         assert z.max() < -80.0, z.max()
         ro, rl = oracle.dense_attention(qq, kk, vv, scale)
         compare_out(o[0, h], ro, lse[0, h], rl, what=f"dense N={n} d={d} h{h}")
+    # the fused search step on the same inputs: O / LSE as K1, and the block masses of every row sum to
+    # the q-block's token count under its exact LSE, however far below zero the logits
+    o2, l2, M, _ = ada.search_select(q, k, v, block_size=block, n_text=0, target=[0.9] * H)
+    torch.cuda.synchronize()
+    blocks = oracle.block_map(n, 0, block, False)
+    L = np.array([b.length for b in blocks], dtype=np.float64)
+    for h in range(H):
+        qq, kk, vv = np64(q[0, h]), np64(k[0, h]), np64(v[0, h])
+        ro, rl = oracle.dense_attention(qq, kk, vv, scale)
+        compare_out(o2[0, h], ro, l2[0, h], rl, what=f"fused N={n} d={d} h{h}")
+        rows = M[0, h].double().cpu().numpy().sum(axis=1) / L
+        assert np.isfinite(rows).all() and np.abs(rows - 1.0).max() <= 1e-5, rows
 
 
 @pytest.mark.parametrize("d", [64, 128])
