@@ -261,7 +261,7 @@ def time_k3_cold(hp, flush, reps=5):
     return stats(out)[0]
 
 
-def kernel_entries(lay, nb, nnz, kfl, med, peaks, traffic, p90=None, heads=None):
+def kernel_entries(lay, nb, nnz, kfl, med, peaks, traffic, p90=None, heads=None, sm_mhz=None):
     """Roofline entries of the path's kernels from per-kernel median ms.  med / p90:
     dicts with keys K1, FS (fused search, optional), K2, K3, K4."""
     tens_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
@@ -288,9 +288,16 @@ def kernel_entries(lay, nb, nnz, kfl, med, peaks, traffic, p90=None, heads=None)
             note="the whole search step t_w in one C-ABI call (adaspa_search_select): dense pass + block "
                  "LSEs (attn_fwd_kernel kModeBlse), block_mass_kernel with the per-row RECALL selection "
                  "epilogue, CSR assembly (head / scan / write)")
-    out["K2_lse_cached_search"] = roofline_entry("alu", N * N * H / (med["K2"] / 1e3) / 1e12, exp_peak, "Texp/s",
+    k2_rate = N * N * H / (med["K2"] / 1e3) / 1e12
+    # K2 sends 1 exponential pair in 8 to an FMA-pipe polynomial (search.cu kSearchPolyMask): the MUFU pipe
+    # itself carries 7/8 of the rate; against its rate at the measured median SM clock of the run
+    mufu_clk = 16.0 * 148 * (sm_mhz or sm_max) * 1e6 / 1e12
+    out["K2_lse_cached_search"] = roofline_entry("alu", k2_rate, exp_peak, "Texp/s",
                                                  traffic.get("K2"), ms=rnd(med["K2"]), ms_p90=rnd(p90.get("K2")),
-                                                 tensor_tflops=round(dense_fl / 2 / (med["K2"] / 1e3) / 1e12, 1))
+                                                 tensor_tflops=round(dense_fl / 2 / (med["K2"] / 1e3) / 1e12, 1),
+                                                 mufu_share=0.875, mufu_frac_at_clock=round(0.875 * k2_rate / mufu_clk, 4),
+                                                 peak_note="MUFU.EX2 16/clk/SM x 148 at sm_max_mhz; frac counts the "
+                                                           "FMA-pipe exponentials too")
     out["K3_select_blocks"] = roofline_entry("hbm", k3_bytes / (med["K3"] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s",
                                              traffic.get("K3"), ms=rnd(med["K3"], 4), ms_p90=rnd(p90.get("K3"), 4))
     out["K4_block_sparse_attn"] = roofline_entry("tensor", kfl / (med["K4"] / 1e3) / 1e12, tens_peak, "TFLOP/s",
@@ -335,7 +342,7 @@ def variant_tiers(hp, q, k, v, lay, peaks, reps=5):
             "head_nnz": [int(x) for x in csr.head_nnz[0].tolist()]}
 
 
-def variant_config(name, args, peaks, traffic, reps=5):
+def variant_config(name, args, peaks, traffic, reps=5, sm_mhz=None):
     """Another BASELINE config (CogVideoX-shaped layer, configs[1]) through the whole hot path:
     per-kernel median ms and roofline."""
     import paper_2502_21079_b200 as ada
@@ -373,7 +380,7 @@ def variant_config(name, args, peaks, traffic, reps=5):
                     "K2": ev[3].elapsed_time(ev[4]), "K3": ev[4].elapsed_time(ev[5])})
     med = {n: stats([p[n] for p in per])[0] for n in per[0]}
     kfl, nnz = kept_flops(lay, hp.csr, lay.head_dim)
-    kern = kernel_entries(lay, hp.nb, nnz, kfl, med, peaks, traffic.get(name, {}))
+    kern = kernel_entries(lay, hp.nb, nnz, kfl, med, peaks, traffic.get(name, {}), sm_mhz=sm_mhz)
     out = {"seq_len": lay.n, "heads": lay.heads, "head_dim": lay.head_dim, "block": lay.block,
            "selection": f"recall {args.recall} per head, text sink",
            "K4_tflops": kern["K4_block_sparse_attn"]["achieved"], "ms_per_layer_sparse": round(med["K4"], 3),
@@ -549,7 +556,8 @@ def run_ours(args):
         variants = {"hyv110k_sparsity0.8_tiers": variant_tiers(hp, q, k, v, lay, peaks)}
         del q, k, v, hp
         torch.cuda.empty_cache()
-        variants["cogx45k_recall0.9"] = variant_config("cogx45k", args, peaks, traffic)
+        variants["cogx45k_recall0.9"] = variant_config("cogx45k", args, peaks, traffic,
+                                                       sm_mhz=(clocks or {}).get("sm_mhz"))
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         qc, kc, vc = workloads.generate_qkv(lay, device=dev)
@@ -563,7 +571,8 @@ def run_ours(args):
     h_max = -(-H // ws)            # K1-K3 times are the slowest rank's, i.e. one with ceil(H/N) heads
     keys = {"K1": I_K1, "FS": I_FS, "K2": I_K2, "K3": I_K3, "K4": I_K4}
     kern = kernel_entries(lay, nb, nnz_all * h_max / H, kfl_all, {n: med[i] for n, i in keys.items()}, peaks,
-                          traffic, p90={n: p90[i] for n, i in keys.items()}, heads=h_max)
+                          traffic, p90={n: p90[i] for n, i in keys.items()}, heads=h_max,
+                          sm_mhz=(clocks or {}).get("sm_mhz"))
     if ws > 1:   # K1-K3 achieved rates per rank's head group; K4 on the whole layer's kept FLOPs
         kern["K4_block_sparse_attn"] = roofline_entry("tensor", value, kern["K4_block_sparse_attn"]["peak"] * ws,
                                                       "TFLOP/s", None, ms=round(med[I_K4], 3),
