@@ -66,7 +66,7 @@ def maybe_spawn(args):
     if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
         return None
     n_dev = torch.cuda.device_count()
-    if n_dev < args.gpus:
+    if n_dev < args.gpus and os.environ.get("ADASPA_BENCH_BACKEND", "nccl") == "nccl":
         print(json.dumps({"error": f"--gpus {args.gpus} but {n_dev} CUDA devices visible"}), flush=True)
         return 2
     import socket
@@ -232,11 +232,21 @@ class _Csr:
         self.row_ptr, self.col_idx = row_ptr, col_idx
 
 
+def local_device(local):
+    """The rank's GPU.  ADASPA_BENCH_BACKEND=gloo (a plumbing check of the multi-rank code paths on a
+    box with fewer GPUs than ranks; its timings mean nothing) lets ranks share devices."""
+    return local % max(1, torch.cuda.device_count())
+
+
 def init_dist(ws, local):
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(local_device(local))
+        backend = os.environ.get("ADASPA_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
 
