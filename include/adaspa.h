@@ -255,6 +255,37 @@ const char* adaspa_status_string(adaspa_status status);
 /* Thread-local message describing the last non-OK status on this thread. */
 const char* adaspa_last_error(void);
 
+/*
+ * Multi-GPU plumbing -- the Ulysses exchange over peer memory (
+ * the method is orthogonal to sequence parallelism).  No arithmetic of the method:
+ * a rank maps every peer's receive buffers into its address space (CUDA IPC), pushes its
+ * head slices into them with copy-engine 2-D copies (NVLink, no SMs), raises one 32-bit flag per
+ * destination, and a consumer's compute stream waits until its flags reach the exchange's epoch.
+ * All calls are asynchronous on `stream` except export / import / close (host calls).  Errors:
+ * ADASPA_ERR_INVALID_ARG (NULL / sizes) or ADASPA_ERR_CUDA; message in adaspa_peer_last_error().
+ */
+typedef struct {
+  uint8_t handle[64];   /* cudaIpcMemHandle_t of the allocation holding the pointer */
+  int64_t offset;       /* byte offset of the pointer inside that allocation        */
+} adaspa_peer_handle;
+
+/* Host: an IPC handle for a device pointer (any pointer inside a cudaMalloc allocation). */
+adaspa_status adaspa_peer_export(const void* dev_ptr, adaspa_peer_handle* out);
+/* Host: map a peer process's pointer; *dev_ptr = mapped pointer, *base = what to pass to close.
+ * Not for a handle exported by the calling process itself (use the local pointer). */
+adaspa_status adaspa_peer_import(const adaspa_peer_handle* in, void** dev_ptr, void** base);
+adaspa_status adaspa_peer_close(void* base);
+/* Stream-ordered 2-D copy between any device pointers the caller can address (local or mapped
+ * peer memory): `rows` rows of `width_bytes`, pitches in bytes (cudaMemcpy2DAsync). */
+adaspa_status adaspa_peer_copy2d(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                                 int64_t width_bytes, int64_t rows, adaspa_stream_t stream);
+/* Stream-ordered write of `value` to a (local or peer) 32-bit flag, after prior work on `stream`. */
+adaspa_status adaspa_peer_signal(uint32_t* flag, uint32_t value, adaspa_stream_t stream);
+/* Later work on `stream` waits until every flags[i] >= value (i < n).  Flags must be device memory
+ * of this process (the peers write them). */
+adaspa_status adaspa_peer_wait(const uint32_t* flags, int32_t n, uint32_t value, adaspa_stream_t stream);
+const char* adaspa_peer_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

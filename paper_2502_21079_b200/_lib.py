@@ -42,8 +42,14 @@ class AttnDesc(ctypes.Structure):
     ]
 
 
+class PeerHandle(ctypes.Structure):
+    """adaspa_peer_handle: CUDA IPC handle of an allocation + the pointer's byte offset in it."""
+    _fields_ = [("handle", ctypes.c_uint8 * 64), ("offset", ctypes.c_int64)]
+
+
 _P = ctypes.c_void_p
 _D = ctypes.POINTER(AttnDesc)
+_PH = ctypes.POINTER(PeerHandle)
 
 SYMBOLS = {
     "adaspa_abi_version": (ctypes.c_int32, []),
@@ -62,6 +68,13 @@ SYMBOLS = {
                                              ctypes.c_size_t, _P]),
     "adaspa_sparse_workspace_bytes": (ctypes.c_size_t, [_D]),
     "adaspa_block_sparse_attn": (ctypes.c_int, [_D, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "adaspa_peer_export": (ctypes.c_int, [_P, _PH]),
+    "adaspa_peer_import": (ctypes.c_int, [_PH, ctypes.POINTER(_P), ctypes.POINTER(_P)]),
+    "adaspa_peer_close": (ctypes.c_int, [_P]),
+    "adaspa_peer_copy2d": (ctypes.c_int, [_P, ctypes.c_int64, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P]),
+    "adaspa_peer_signal": (ctypes.c_int, [_P, ctypes.c_uint32, _P]),
+    "adaspa_peer_wait": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_uint32, _P]),
+    "adaspa_peer_last_error": (ctypes.c_char_p, []),
     "adaspa_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "adaspa_last_error": (ctypes.c_char_p, []),
 }
@@ -317,3 +330,44 @@ def block_sparse_attn(q, k, v, row_ptr, col_idx, *, block_size, n_text, text_fir
                                          _ptr(col_idx), _ptr(o), _ptr(lse), _ptr(workspace), workspace.numel(),
                                          _stream(stream)), "adaspa_block_sparse_attn")
     return o, lse
+
+
+# ---------------------------------------------------------------- peer-memory plumbing (multi-GPU)
+def _peer_check(status, where):
+    if status != OK:
+        raise RuntimeError(f"{where}: {_lib.adaspa_status_string(status).decode()}: "
+                           f"{_lib.adaspa_peer_last_error().decode()}")
+
+
+def peer_export(ptr):
+    """IPC handle (bytes) of a device pointer: CUDA IPC handle of its allocation + the byte offset."""
+    h = PeerHandle()
+    _peer_check(_lib.adaspa_peer_export(ctypes.c_void_p(ptr), ctypes.byref(h)), "adaspa_peer_export")
+    return bytes(h.handle) + int(h.offset).to_bytes(8, "little", signed=True)
+
+
+def peer_import(blob):
+    """Map a peer process's exported pointer: returns (device pointer, base to close)."""
+    h = PeerHandle()
+    ctypes.memmove(h.handle, blob[:64], 64)
+    h.offset = int.from_bytes(blob[64:72], "little", signed=True)
+    ptr, base = ctypes.c_void_p(), ctypes.c_void_p()
+    _peer_check(_lib.adaspa_peer_import(ctypes.byref(h), ctypes.byref(ptr), ctypes.byref(base)), "adaspa_peer_import")
+    return ptr.value, base.value
+
+
+def peer_close(base):
+    _peer_check(_lib.adaspa_peer_close(ctypes.c_void_p(base)), "adaspa_peer_close")
+
+
+def peer_copy2d(dst, dst_pitch, src, src_pitch, width, rows, stream=None):
+    _peer_check(_lib.adaspa_peer_copy2d(ctypes.c_void_p(dst), dst_pitch, ctypes.c_void_p(src), src_pitch, width, rows,
+                                        _stream(stream)), "adaspa_peer_copy2d")
+
+
+def peer_signal(flag_ptr, value, stream=None):
+    _peer_check(_lib.adaspa_peer_signal(ctypes.c_void_p(flag_ptr), value, _stream(stream)), "adaspa_peer_signal")
+
+
+def peer_wait(flags_ptr, n, value, stream=None):
+    _peer_check(_lib.adaspa_peer_wait(ctypes.c_void_p(flags_ptr), n, value, _stream(stream)), "adaspa_peer_wait")

@@ -243,3 +243,145 @@ def reduce_step_timings(kernel_ms, kept_flops, steps, group=None):
     w = reduce_sum([kept_flops], group)[0]
     value = w * steps / (t[4] / 1e3) / 1e12
     return value, t
+
+
+def _runs(heads):
+    """Maximal runs of consecutive head ids in a head list: (first head, count, position in the list)."""
+    out, i = [], 0
+    while i < len(heads):
+        j = i
+        while j + 1 < len(heads) and heads[j + 1] == heads[j] + 1:
+            j += 1
+        out.append((heads[i], j - i + 1, i))
+        i = j + 1
+    return out
+
+
+class PeerExchange:
+    """The Ulysses exchange over peer memory instead of NCCL.
+
+    Every rank owns receive buffers -- `n_in` head-sharded tensors [N, H_r, d] (Q, K, V of its head
+    set, token-major as the kernels read them) and one sequence-sharded [N_p, H, d] (O of its token
+    chunk) -- plus a flag block [4, world] (in-ready, in-released, out-ready, out-released; slot p is
+    written by rank p).  The buffers are CUDA IPC-mapped into every other rank once (handles
+    exchanged with one all_gather_object).  A push is copy-engine 2-D copies straight into the
+    destinations' buffers (each contiguous run of a destination's head list is one copy per tensor:
+    rows = this rank's tokens, pitches H*d and H_r*d) followed by one 32-bit flag write per
+    destination, all stream-ordered on the caller's stream; `wait_*` makes the caller's stream wait
+    until every peer's flag reaches the exchange's epoch.  Before overwriting a destination's buffer
+    a push waits for that destination's release of the previous epoch (`release_*`, recorded after
+    the kernels that read the buffer), so exchanges can be issued ahead of compute.  No NCCL and no
+    SMs on the data path; nothing of the method's arithmetic.  At world size 1 the "peer" is this
+    process (local pointers, no IPC)."""
+
+    IN_READY, IN_REL, OUT_READY, OUT_REL = range(4)
+
+    def __init__(self, N, H, d, sizes, assign, device, group=None, n_in=3, dtype=torch.bfloat16):
+        from . import _lib as L
+        self._L = L
+        self.world = _world(group)
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        if sorted(h for a in assign for h in a) != list(range(H)) or len(assign) != self.world:
+            raise ValueError("assign must partition the heads over the ranks")
+        if len(sizes) != self.world or sum(sizes) != N:
+            raise ValueError("sizes must give every rank's token count")
+        self.N, self.H, self.d, self.sizes, self.assign = N, H, d, list(sizes), [list(a) for a in assign]
+        self.offs = [sum(sizes[:r]) for r in range(self.world)]
+        self.es = torch.empty(0, dtype=dtype).element_size()
+        Hr = len(assign[self.rank])
+        self.recv_in = [torch.empty(N, Hr, d, dtype=dtype, device=device) for _ in range(n_in)]
+        self.recv_out = torch.empty(sizes[self.rank], H, d, dtype=dtype, device=device)
+        self.flags = torch.zeros(4, self.world, dtype=torch.int32, device=device)
+        self.n_in = n_in
+        mine = [t.data_ptr() for t in self.recv_in] + [self.recv_out.data_ptr(), self.flags.data_ptr()]
+        self._bases = []
+        if self.world == 1:
+            ptrs = [mine]
+        else:
+            torch.cuda.synchronize(device)
+            blobs = [L.peer_export(p) for p in mine]
+            every = [None] * self.world
+            dist.all_gather_object(every, blobs, group=group)
+            ptrs = []
+            for r in range(self.world):
+                if r == self.rank:
+                    ptrs.append(mine)
+                    continue
+                row = []
+                for b in every[r]:
+                    p, base = L.peer_import(b)
+                    row.append(p)
+                    self._bases.append(base)
+                ptrs.append(row)
+        self.peer_in = [row[:n_in] for row in ptrs]
+        self.peer_out = [row[n_in] for row in ptrs]
+        self.peer_flags = [row[n_in + 1] for row in ptrs]
+        self.epoch_in = 0
+        self.epoch_out = 0
+
+    def close(self):
+        for b in self._bases:
+            self._L.peer_close(b)
+        self._bases = []
+
+    def _flag(self, r, kind, slot):
+        return self.peer_flags[r] + 4 * (kind * self.world + slot)
+
+    def _own_flags(self, kind):
+        return self.flags.data_ptr() + 4 * kind * self.world
+
+    def push_in(self, xs, stream=None):
+        """This rank's token chunks [N_p, H, d] (one per input tensor, contiguous) into every rank's
+        head-sharded receive buffers; raises IN_READY on each destination."""
+        L, es, d, H = self._L, self.es, self.d, self.H
+        Np = self.sizes[self.rank]
+        if len(xs) != self.n_in or any(tuple(x.shape) != (Np, H, d) or not x.is_contiguous() for x in xs):
+            raise ValueError(f"push_in needs {self.n_in} contiguous [{Np}, {H}, {d}] tensors")
+        e = self.epoch_in + 1
+        # the destinations must have released epoch e-1 of their buffers
+        L.peer_wait(self._own_flags(self.IN_REL), self.world, e - 1, stream)
+        for r in range(self.world):
+            Hr = len(self.assign[r])
+            for h0, n, pos in _runs(self.assign[r]):
+                for i, x in enumerate(xs):
+                    L.peer_copy2d(self.peer_in[r][i] + (self.offs[self.rank] * Hr + pos) * d * es, Hr * d * es,
+                                  x.data_ptr() + h0 * d * es, H * d * es, n * d * es, Np, stream)
+            L.peer_signal(self._flag(r, self.IN_READY, self.rank), e, stream)
+        self.epoch_in = e
+
+    def wait_in(self, stream=None):
+        """Later work on `stream` waits until every rank's push of this epoch has landed; returns
+        the receive buffers [N, H_r, d]."""
+        self._L.peer_wait(self._own_flags(self.IN_READY), self.world, self.epoch_in, stream)
+        return self.recv_in
+
+    def release_in(self, stream=None):
+        """After the kernels that read recv_in (stream-ordered): lets the next push overwrite them."""
+        for r in range(self.world):
+            self._L.peer_signal(self._flag(r, self.IN_REL, self.rank), self.epoch_in, stream)
+
+    def push_out(self, o_heads, stream=None):
+        """O of this rank's head set [N, H_r, d] (token-major) back to every rank's [N_p, H, d] buffer
+        (heads in their global order); raises OUT_READY on each destination."""
+        L, es, d, H = self._L, self.es, self.d, self.H
+        mine = self.assign[self.rank]
+        Hr = len(mine)
+        if tuple(o_heads.shape) != (self.N, Hr, d) or o_heads.stride() != (Hr * d, d, 1):
+            raise ValueError(f"push_out needs a [{self.N}, {Hr}, {d}] token-major tensor")
+        e = self.epoch_out + 1
+        L.peer_wait(self._own_flags(self.OUT_REL), self.world, e - 1, stream)
+        for p in range(self.world):
+            for h0, n, pos in _runs(mine):
+                L.peer_copy2d(self.peer_out[p] + h0 * d * es, H * d * es,
+                              o_heads.data_ptr() + (self.offs[p] * Hr + pos) * d * es, Hr * d * es, n * d * es,
+                              self.sizes[p], stream)
+            L.peer_signal(self._flag(p, self.OUT_READY, self.rank), e, stream)
+        self.epoch_out = e
+
+    def wait_out(self, stream=None):
+        self._L.peer_wait(self._own_flags(self.OUT_READY), self.world, self.epoch_out, stream)
+        return self.recv_out
+
+    def release_out(self, stream=None):
+        for r in range(self.world):
+            self._L.peer_signal(self._flag(r, self.OUT_REL, self.rank), self.epoch_out, stream)

@@ -26,7 +26,7 @@ def lib():
 
 def test_exports_every_header_symbol(lib):
     names = _header_functions()
-    assert len(names) == 14, names
+    assert len(names) == 20, names
     for n in names:
         assert hasattr(lib._lib, n), n
         assert n in lib.SYMBOLS, n
@@ -174,3 +174,18 @@ def test_search_select_needs_block_mass_above_2048_blocks(lib):
     st = L.adaspa_search_select(ctypes.byref(d), fake, fake, fake, fake, fake, nul, tg, 1, fake, fake, nb * nb,
                                 nul, nul, nul, fake, ws, nul)
     assert st == lib.ERR_INVALID_ARG and b"2048" in L.adaspa_last_error()
+
+
+def test_peer_plumbing_rejects_bad_arguments(lib):
+    """The peer-memory exchange entries reject NULL / inconsistent arguments before touching CUDA."""
+    L = lib._lib
+    nul = ctypes.c_void_p(0)
+    fake = ctypes.c_void_p(0x10000)
+    assert L.adaspa_peer_export(nul, None) == lib.ERR_INVALID_ARG
+    assert L.adaspa_peer_import(None, None, None) == lib.ERR_INVALID_ARG
+    assert L.adaspa_peer_close(nul) == lib.ERR_INVALID_ARG
+    assert L.adaspa_peer_copy2d(fake, 16, fake, 16, 32, 4, nul) == lib.ERR_INVALID_ARG   # pitch < width
+    assert L.adaspa_peer_copy2d(fake, 64, fake, 64, 0, 4, nul) == lib.OK                  # empty copy: no-op
+    assert L.adaspa_peer_signal(nul, 1, nul) == lib.ERR_INVALID_ARG
+    assert L.adaspa_peer_wait(nul, 2, 1, nul) == lib.ERR_INVALID_ARG
+    assert b"flags" in L.adaspa_peer_last_error()
