@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--ulysses", action="store_true",
                     help="BASELINE configs[3]: sequence-sharded activations, NCCL all-to-all to head shards "
                          "and back around the search step and around the sparse step (strong scaling)")
+    ap.add_argument("--p2p", action="store_true",
+                    help="with --ulysses: the exchange over peer memory (dist.PeerExchange: IPC-mapped buffers, "
+                         "copy-engine copies, stream-ordered flags) instead of NCCL all-to-all")
     return ap.parse_args()
 
 
@@ -641,9 +644,13 @@ def run_ulysses(args):
     the whole layer / max over ranks of the K4 time (strong scaling)."""
     ws, rank, local = dist_env()
     import torch.distributed as dist
+    local = local_device(local)
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("ADASPA_BENCH_BACKEND", "nccl") == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:   # plumbing check with ranks sharing a GPU (needs --p2p: gloo has no CUDA all_to_all)
+            dist.init_process_group(os.environ["ADASPA_BENCH_BACKEND"])
     else:
         import socket
         so = socket.socket()
@@ -683,15 +690,35 @@ def run_ulysses(args):
     mine = assign[rank]
     del sh
     ws4 = None
+    ex_s = ex_4 = None
+    if args.p2p:   # peer-memory exchange: one for the search step's head groups, one for the sparse step's
+        ex_s = D.PeerExchange(N, H, d, sizes, contig, dev)
+        ex_4 = D.PeerExchange(N, H, d, sizes, assign, dev)
+
+    def a2a_in(ex, asg):
+        if ex is None:
+            return [D.as_bhnd(D.ulysses_in(x, sizes=sizes, assign=asg)) for x in loc]
+        ex.push_in(loc)
+        return [D.as_bhnd(x) for x in ex.wait_in()]
+
+    def a2a_out(ex, o_tok, asg):
+        if ex is None:
+            return D.ulysses_out(o_tok, sizes, assign=asg)
+        ex.push_out(o_tok)
+        out = ex.wait_out()
+        ex.release_out()
+        return out
 
     def step(ev=None):
         rec = (lambda i: ev[i].record()) if ev else (lambda i: None)  # noqa: E731
         nonlocal ws4
         rec(0)
-        sh = [D.as_bhnd(D.ulysses_in(x, sizes=sizes)) for x in loc]             # [1, Hp, N, d] token-major views
+        sh = a2a_in(ex_s, contig)                                               # [1, Hp, N, d] token-major views
         rec(1)
         hp.search(*sh, events=ev[1:5] if ev else None)
-        o_d = D.ulysses_out(hp.o_dense[0].transpose(0, 1), sizes)               # O of the search step back
+        if ex_s is not None:
+            ex_s.release_in()
+        o_d = a2a_out(ex_s, hp.o_dense[0].transpose(0, 1), contig)              # O of the search step back
         rec(5)
         if args.lpt:
             rp, ci = D.gather_csr(hp.csr.row_ptr, hp.csr.col_idx)
@@ -699,15 +726,17 @@ def run_ulysses(args):
         else:
             csr = hp.csr
         rec(6)
-        s4 = [D.as_bhnd(D.ulysses_in(x, sizes=sizes, assign=assign)) for x in loc]   # sparse step's a2a in
+        s4 = a2a_in(ex_4, assign)                                               # sparse step's a2a in
         rec(7)
         if ws4 is None:
             ws4 = torch.empty(max(ada.sparse_workspace_bytes(ada.make_desc(s4[0], **kw)), 1), dtype=torch.uint8,
                               device=dev)
-        o4 = torch.empty_like(s4[0])
+        o4 = torch.empty(1, N, len(mine), d, dtype=s4[0].dtype, device=dev).transpose(1, 2)   # token-major
         ada.block_sparse_attn(*s4, csr.row_ptr, csr.col_idx, o=o4, workspace=ws4, **kw)
+        if ex_4 is not None:
+            ex_4.release_in()
         rec(8)
-        o_s = D.ulysses_out(o4[0].transpose(0, 1), sizes, assign=assign)
+        o_s = a2a_out(ex_4, o4[0].transpose(0, 1), assign)
         rec(9)
         step.csr = csr
         return o_d, o_s
@@ -743,7 +772,8 @@ def run_ulysses(args):
             "data": "synthetic (workloads/synth.py, seeded; DESIGN.md §5)",
             "config": {"workload": lay.name + "-ulysses", "seq_len": N, "heads": H, "heads_per_rank": Hp,
                        "head_dim": d, "block": lay.block,
-                       "parallelism": f"ulysses a2a x{ws} (NCCL)" + (" + LPT sparse-step head sets" if args.lpt else ""),
+                       "parallelism": f"ulysses a2a x{ws} " + ("(peer memory: IPC + copy engines)" if args.p2p else "(NCCL)")
+                                      + (" + LPT sparse-step head sets" if args.lpt else ""),
                        "l2": "inputs larger than L2"},
             "ms_per_layer_sparse": round(ms[7], 3), "t_w_search_step_ms": round(ms[1] + ms[2] + ms[3], 3),
             "a2a_ms": {"search_in": round(ms[0], 3), "search_out": round(ms[4], 3), "sparse_in": round(ms[6], 3),
