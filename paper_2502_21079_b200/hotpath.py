@@ -51,6 +51,7 @@ class HotPath:
                          e(batch, heads, dt=torch.float32), e(batch, heads, dt=torch.int64))
         self.ws = e(max(L.sparse_workspace_bytes(self.desc), 1), dt=torch.uint8)
         self.fws = None     # fused-search scratch (K3 workspace + 4*(nb+1)*N bytes per head), on first use
+        self.heads_per_pass = 0   # fused search: heads per dense pass (0: all; fewer bound the scratch)
         self.mass2 = None   # block masses of a later key step (K2 with the cached LSE)
 
     def _stage(self, q, k, v):
@@ -77,8 +78,8 @@ class HotPath:
         rec(0)
         if fused is True:
             if self.fws is None:
-                self.fws = torch.empty(L.search_select_workspace_bytes(self.desc, 0), dtype=torch.uint8,
-                                       device=self.device)
+                self.fws = torch.empty(L.search_select_workspace_bytes(self.desc, self.heads_per_pass),
+                                       dtype=torch.uint8, device=self.device)
             L.search_select(q, k, v, target=self.targets, flags=self.flags, o=self.o_dense, lse=self.lse,
                             block_mass=self.mass, out=self.csr, workspace=self.fws, **self.kw)
             rec(1)
@@ -87,8 +88,8 @@ class HotPath:
             return self.csr
         if fused:
             if self.fws is None:
-                self.fws = torch.empty(L.search_select_workspace_bytes(self.desc, 0), dtype=torch.uint8,
-                                       device=self.device)
+                self.fws = torch.empty(L.search_select_workspace_bytes(self.desc, self.heads_per_pass),
+                                       dtype=torch.uint8, device=self.device)
             L.dense_attn_lse_search(q, k, v, o=self.o_dense, lse=self.lse, block_mass=self.mass,
                                     workspace=self.fws, **self.kw)
             rec(1)
