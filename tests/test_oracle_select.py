@@ -187,3 +187,48 @@ def test_schedule_golden(golden_dir):
     assert oracle.schedule_trace(20, 5, [5]).count("cached-search+sparse") == 0
     with pytest.raises(ValueError):
         oracle.schedule_trace(50, 10, [12, 30])
+
+
+def test_head_recall_equals_token_level_recall():
+    """Independent pin of the whole-matrix Recall (the share of the attention weight
+    matrix A that the mask keeps): computed at TOKEN level from an explicit softmax matrix (torch,
+    fp64) with the block mask expanded to tokens, it must equal what select_blocks reports from the
+    block masses."""
+    import torch
+    rng = np.random.default_rng(5)
+    nv, nt, B, d, H = 70, 13, 8, 16, 2
+    blocks = oracle.block_map(nv, nt, B, False)
+    N = nv + nt
+    scale = 1 / math.sqrt(d)
+    q = rng.standard_normal((H, N, d)) * 1.5
+    k = rng.standard_normal((H, N, d)) * 1.5
+    M = np.stack([oracle.block_mass(q[h], k[h], np.log(np.exp(scale * q[h] @ k[h].T).sum(axis=1)), blocks, scale)
+                  for h in range(H)])
+    keep, rec, _, _ = oracle.select_blocks(M, blocks, "recall", [0.7, 0.95], text_sink=True)
+    for h in range(H):
+        A = torch.softmax(torch.tensor(scale * q[h] @ k[h].T, dtype=torch.float64), dim=-1).numpy()
+        tok = np.zeros((N, N), dtype=bool)
+        for p, bp in enumerate(blocks):
+            for j, bj in enumerate(blocks):
+                if keep[h, p, j]:
+                    tok[bp.start:bp.start + bp.length, bj.start:bj.start + bj.length] = True
+        assert abs((A * tok).sum() / A.sum() - rec[h]) < 1e-12
+
+
+def test_tiers_composition_hand_example():
+    """The tiered selection worked by hand from PAPER.md:527-533 (readings R11, R16, R17) on two
+    heads with one 4-block row each (no text):
+      head 0 masses [0.75, 0.10, 0.10, 0.05], head 1 [0.25]*4, base sparsity s = 0.5;
+      base k = floor(0.5*4 + 0.5 + 1e-9) = 2 -> Recall 0.85 (head 0) and 0.50 (head 1);
+      n = min(#{R > 0.8} = 1, floor(2/2) = 1): head 0 -> (1+s)/2 = 0.75, head 1 -> (3s-1)/2 = 0.25;
+      k = floor(0.25*4 + 0.5) = 1 (head 0 keeps block 0) and floor(0.75*4 + 0.5) = 3 (head 1 keeps
+      blocks 0, 1, 2: equal masses, ids ascending, R10)."""
+    blocks = oracle.block_map(4 * 8, 0, 8, False)
+    M = np.array([[[0.75, 0.10, 0.10, 0.05]] * 4, [[0.25] * 4] * 4])
+    keep, rec, nnz, tg = oracle.select_blocks(M, blocks, "sparsity", [0.5, 0.5], tiers=True)
+    assert tg == pytest.approx([0.75, 0.25])
+    for p in range(4):
+        assert keep[0, p].tolist() == [True, False, False, False]
+        assert keep[1, p].tolist() == [True, True, True, False]
+    assert rec[0] == pytest.approx(0.75) and rec[1] == pytest.approx(0.75)
+    assert nnz.tolist() == [4, 12]
