@@ -63,7 +63,15 @@ __device__ int g_trace_n[2];
 
 namespace {
 
-constexpr int kThreads = 640;
+constexpr int kThreads = 640;  // d=64: 4 + 16 softmax warps (16 rows per warp)
+#ifndef ADASPA_ROW_THREAD
+#define ADASPA_ROW_THREAD 1
+#endif
+// d=128: one S row per softmax thread (4 + 8 warps), see the kRowThread softmax below
+template <int D>
+constexpr bool row_thread() { return D == 128 && ADASPA_ROW_THREAD != 0; }
+template <int D>
+constexpr int threads_of() { return row_thread<D>() ? 384 : kThreads; }
 __device__ __forceinline__ uint32_t s_col(int t) { return static_cast<uint32_t>(t) * 128u; }
 __device__ __forceinline__ uint32_t o_col(int t) { return 256u + static_cast<uint32_t>(t) * 128u; }
 // d=64: O_t uses 64 of its 128 columns, so P_t gets the other 64 instead of aliasing S_t.  The next
@@ -85,9 +93,6 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define ADASPA_ABLATE 0  // diagnostic builds only: 4 = no softmax (MMA / TMA pipeline alone)
 #endif
 constexpr int kExpPolyMod = ADASPA_EXP_POLY_MOD;
-#ifndef ADASPA_ARRIVE_RELAXED
-#define ADASPA_ARRIVE_RELAXED 0
-#endif
 #ifndef ADASPA_BLSE_ABL
 #define ADASPA_BLSE_ABL 0  // diagnostic builds only: 1 = no per-tile block-LSE epilogue, 2 = no store
 #endif
@@ -186,7 +191,7 @@ static_assert(Smem<128>::kBytes <= 232448 && Smem<64>::kBytes <= 232448, "over 2
 // log-sum-exp is written for the fused block-mass reduction), kSparse (K4: the merged CSR stream).
 // QTWO: a q tile is two 64-row q-blocks (sparse B=64); KVTWO: a kv tile is two 64-row kv blocks.
 template <int D, bool QTWO, bool KVTWO, int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(threads_of<D>(), 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, const AttnParams p) {
   constexpr bool SPARSE = MODE == kModeSparse;
@@ -195,6 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // skip the exponentials of fully masked 64-column halves: only where they are common (the B=64
   // pairs of the sparse stream); elsewhere the branch costs registers for nothing
   constexpr bool kSkipDead = SPARSE && KVTWO;
+  constexpr bool kRowThread = row_thread<D>();
+  constexpr int kSoftWarps = kRowThread ? 4 : 8;  // softmax warps per q tile
   using S = Smem<D>;
   constexpr int NS = S::kNS;
   constexpr bool kSepP = D == 64;
@@ -223,12 +230,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars->q_empty, kIssuers);
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bars->s_full[t], 2);
-      mbar_init(&bars->p_half[t], 8);  // P columns [0, 32) (kv rows 0-63) of every row stored
-      mbar_init(&bars->p_full[t], 8);
-      mbar_init(&bars->s_loaded[t], 8);
+      mbar_init(&bars->p_half[t], kSoftWarps);  // P columns [0, 32) (kv rows 0-63) of every row stored
+      mbar_init(&bars->p_full[t], kSoftWarps);
+      mbar_init(&bars->s_loaded[t], kSoftWarps);
       mbar_init(&bars->p_free[t], 1);
       mbar_init(&bars->o_full[t], 1);
-      mbar_init(&bars->o_empty[t], 8);
+      mbar_init(&bars->o_empty[t], kSoftWarps);
     }
     fence_mbar_init();
     tma_prefetch_desc(&tq);
@@ -247,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // softmax warpgroups, which hold a 64-column half S row each.  The pool is what the launch
   // allocated, 640 x 96: 64*128 + 104*512 = 61440 (setmaxnreg.inc beyond it never returns).
   if (warp < 4) {
-  regs_dec<64>();
+  if constexpr (kRowThread) regs_dec<80>(); else regs_dec<64>();
   if (warp == 0) {
     // ============================================================ TMA producer
     if (lane == 0) {
@@ -557,6 +564,220 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  } else if constexpr (kRowThread) {
+    // 384 threads x 168 registers at launch (64512); the producer/MMA warpgroup drops to 80 (its MMA
+    // issuer spills at 64 here), so the two softmax warpgroups take (64512 - 4*32*80) / 256 = 212 ->
+    // 208 each: a whole 128-column S row (128 registers) per thread
+    regs_inc<208>();
+    // ============================================================ softmax warps, one row per thread
+    // warps 4..11: q tile t = (warp - 4) >> 2; warp lane quarter wq = warp & 3 owns TMEM lanes
+    // [32 wq, 32 wq + 32); thread = one row of the tile with all 128 columns (32x32b TMEM shapes).
+    // The row max, the row sum and the per-block sums of the fused search are thread-local: no
+    // shuffles, no votes; four warps per q tile arrive on each hand-off.
+    const int t = (warp - 4) >> 2;
+    const int wq = warp & 3;
+    const int hq = wq >> 1;  // 64-row half of the q tile (column-limit index)
+    const int row = wq * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+    const uint32_t s_addr = tmem + lane_base + s_col(t);
+    const uint32_t o_addr = tmem + lane_base + o_col(t);
+    const uint32_t p_addr = tmem + lane_base + p_col<D>(t);  // d=128: P over S columns [0, 64)
+    const float sl2 = p.scale_log2;
+    uint32_t sph = 0, oph = 0;
+    int icnt = 0;
+    float m_used = -INFINITY;  // running max (log2 units), moved only when the row max passes it by 8
+    float l_sum = 0.0f;
+    float ref = 0.0f;          // BLSE: the row's first running max
+    int ntile = 0;
+    float* blse_row = nullptr;  // BLSE: this row of the block-LSE scratch (per item)
+    bool blse_ok = false;
+    for (;;) {
+      mbar_wait(&bars->s_full[t], sph);
+      sph ^= 1;
+      tc_fence_after();
+      const TileInfo& inf = bars->info[t][icnt & 1];
+      ++icnt;
+      const int kind = inf.kind;
+      if (kind == kAllEnd) break;
+      if (kind == kEnd) {
+        const int b = inf.b, h = inf.h;
+        int tok;
+        bool valid;
+        if (!QTWO || row < 64) {
+          tok = inf.start0 + row;
+          valid = row < inf.len0;
+        } else {
+          tok = inf.start1 + row - 64;
+          valid = row - 64 < inf.len1;
+        }
+        __nv_bfloat16* optr = p.o + b * p.sb + h * p.sh + static_cast<int64_t>(valid ? tok : 0) * p.sn;
+        if (inf.has) {
+          // a row with at least one kept column has l >= 1 (the element that set m contributes 2^0)
+          const float inv = l_sum >= 0.25f ? 1.0f / l_sum : 0.0f;
+          mbar_wait(&bars->o_full[t], oph);
+          oph ^= 1;
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(o_addr + c * 32, r);
+            tmem_ld_wait32(r);
+            uint4 w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              w[i] = make_uint4(pack_bf16x2(__uint_as_float(r[8 * i + 0]) * inv, __uint_as_float(r[8 * i + 1]) * inv),
+                                pack_bf16x2(__uint_as_float(r[8 * i + 2]) * inv, __uint_as_float(r[8 * i + 3]) * inv),
+                                pack_bf16x2(__uint_as_float(r[8 * i + 4]) * inv, __uint_as_float(r[8 * i + 5]) * inv),
+                                pack_bf16x2(__uint_as_float(r[8 * i + 6]) * inv, __uint_as_float(r[8 * i + 7]) * inv));
+            if (valid) {
+              uint4* dst = reinterpret_cast<uint4*>(optr + 32 * c);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) dst[i] = w[i];
+            }
+          }
+          if (valid && p.lse)
+            p.lse[(static_cast<int64_t>(b) * p.H + h) * p.N + tok] =
+                l_sum >= 0.25f ? (m_used + __log2f(l_sum)) * kLn2 : -INFINITY;
+          if (BLSE && valid)  // the row LSE relative to ref (log2 units), for the block-mass reduction
+            p.lrel[(static_cast<int64_t>(b) * p.nh + (h - p.h0)) * p.N + tok] =
+                l_sum >= 0.25f ? (m_used - ref) + __log2f(l_sum) : -INFINITY;
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars->o_empty[t]);
+        } else {  // no kept kv block for any row of this tile (a caller CSR with empty rows)
+          if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(optr);
+#pragma unroll
+            for (int i = 0; i < D / 8; ++i) dst[i] = make_uint4(0u, 0u, 0u, 0u);
+            if (p.lse) p.lse[(static_cast<int64_t>(b) * p.H + h) * p.N + tok] = -INFINITY;
+          }
+        }
+        m_used = -INFINITY;
+        l_sum = 0.0f;
+        ref = 0.0f;
+        ntile = 0;
+        continue;
+      }
+      const int limA = *reinterpret_cast<const volatile int*>(&inf.lim[hq * 2 + 0]);
+      const int limB = *reinterpret_cast<const volatile int*>(&inf.lim[hq * 2 + 1]);
+      if (BLSE && ntile == 0) {  // per item: this row in blse[b,h][kb][.] and whether it stores
+        const int64_t bhl = static_cast<int64_t>(inf.b) * p.nh + (inf.h - p.h0);
+        blse_row = p.blse + bhl * p.grid.nb * p.N + inf.start0 + row;
+        blse_ok = row < inf.len0;
+      }
+      uint32_t s[128];
+      tmem_ld32(s_addr, s);
+      tmem_ld32(s_addr + 32, s + 32);
+      tmem_ld32(s_addr + 64, s + 64);
+      tmem_ld32(s_addr + 96, s + 96);
+      tmem_ld_wait();
+      reg_fence32(s);
+      reg_fence32(s + 32);
+      reg_fence32(s + 64);
+      reg_fence32(s + 96);
+      // dead halves (kSkipDead: masked for every row of the warp) skip their exponentials and stay
+      // out of the max; a partial block (or an unneeded half without kSkipDead) is masked to -inf
+      const bool deadA = kSkipDead && limA == 0, deadB = kSkipDead && limB <= 64;
+      if ((limA < 64 && !deadA) || (limB < 128 && !deadB)) {
+#pragma unroll
+        for (int i = 0; i < 128; ++i) {
+          const int lim = i < 64 ? limA : limB;
+          s[i] = i < lim ? s[i] : __float_as_uint(-INFINITY);
+        }
+      }
+      float mx0 = fmaxf(__uint_as_float(s[0]), __uint_as_float(s[1]));
+      float mx1 = fmaxf(__uint_as_float(s[2]), __uint_as_float(s[3]));
+      float mx2 = fmaxf(__uint_as_float(s[64]), __uint_as_float(s[65]));
+      float mx3 = fmaxf(__uint_as_float(s[66]), __uint_as_float(s[67]));
+#pragma unroll
+      for (int i = 4; i < 64; i += 4) {
+        mx0 = fmax3(mx0, __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
+        mx1 = fmax3(mx1, __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
+        mx2 = fmax3(mx2, __uint_as_float(s[64 + i]), __uint_as_float(s[65 + i]));
+        mx3 = fmax3(mx3, __uint_as_float(s[66 + i]), __uint_as_float(s[67 + i]));
+      }
+      const float mxa = deadA ? -INFINITY : fmaxf(mx0, mx1), mxb = deadB ? -INFINITY : fmaxf(mx2, mx3);
+      const float mx = fmaxf(mxa, mxb) * sl2;
+      float alpha = 1.0f;
+      bool rescale = false;
+      if (mx > m_used + kRescaleThreshold) {  // also true when m_used == -inf (and mx finite)
+        alpha = (m_used == -INFINITY) ? 0.0f : exp2f(m_used - mx);
+        l_sum *= alpha;
+        if (BLSE && m_used == -INFINITY) ref = mx;
+        m_used = mx;
+        rescale = alpha != 0.0f && ntile > 0;
+      }
+      if (__any_sync(0xffffffffu, rescale)) {  // rare: some row's max grew by more than 2^8
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(o_addr + c * 32, r);
+          tmem_ld_wait32(r);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+          tmem_st32(o_addr + c * 32, r);
+        }
+      }
+      const float mb = (m_used == -INFINITY) ? 0.0f : m_used;
+      // P = 2^(S*scale*log2e - m): FFMA2 for the argument, MUFU.EX2, packed to bf16 pairs: S columns
+      // 2j, 2j+1 -> P column j (the TS MMA's A layout)
+      const float2 sl2v = make_float2(sl2, sl2);
+      const float2 nm = make_float2(-mb, -mb);
+      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      float half0 = 0.0f;  // the row sum over columns 0-63 (BLSE with KVTWO: kv block id0)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t pk[32];
+        const bool dead = c == 0 ? deadA : deadB;
+        if (dead) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) pk[i] = 0u;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const int i = 64 * c + 2 * k;
+            const float2 x = ffma2(make_float2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sl2v, nm);
+            float2 e;
+            e.x = ex2_approx(x.x);
+            e.y = ex2_approx(x.y);
+            acc[k & 3] = fadd2(acc[k & 3], e);
+            pk[k] = pack_bf16x2(e.x, e.y);
+          }
+        }
+        tmem_st32(p_addr + c * 32, pk);
+        if (c == 0) {  // first half of P stored: the MMA thread may start PV on kv rows 0-63
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars->p_half[t]);
+          const float2 h01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+          half0 = h01.x + h01.y;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[i] = make_float2(0.f, 0.f);
+        }
+      }
+      const float2 h23 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+      const float half1 = h23.x + h23.y;
+      l_sum += half0 + half1;
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->p_full[t]);
+      if (BLSE && blse_ok) {
+        // this tile's per-block log-sum-exps relative to the row's first max (thread-local sums):
+        // log2 sum_{j in kb} 2^(s_ij*scale*log2e) - ref = log2(t) + (m_used - ref); tile n is block n
+        // (KVTWO: blocks 2n and 2n+1); tt = 0 gives -inf
+        const float mref = m_used - ref;
+        if (KVTWO) {
+          __stcs(blse_row + static_cast<int64_t>(2 * ntile) * p.N, __log2f(half0) + mref);
+          if (2 * ntile + 1 < p.grid.nb)
+            __stcs(blse_row + static_cast<int64_t>(2 * ntile + 1) * p.N, __log2f(half1) + mref);
+        } else {
+          __stcs(blse_row + static_cast<int64_t>(ntile) * p.N, __log2f(half0 + half1) + mref);
+        }
+      }
+      ++ntile;
+    }
   } else {
     regs_inc<104>();
     // ============================================================ softmax warps
@@ -928,9 +1149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) {
-            if (ADASPA_ARRIVE_RELAXED) mbar_arrive_relaxed(&bars->p_half[t]); else mbar_arrive(&bars->p_half[t]);
-          }
+          if (lane == 0) mbar_arrive(&bars->p_half[t]);
           if (BLSE && KVTWO) {  // kv block id0 ends here: keep its row sums apart from block id1's
             const float2 h0 = fadd2(acc[0], acc[2]), h1 = fadd2(acc[1], acc[3]);
             half0[0] = h0.x + h0.y;
@@ -948,9 +1167,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       ADASPA_TRACE_EV(3);
-      if (lane == 0) {
-        if (ADASPA_ARRIVE_RELAXED) mbar_arrive_relaxed(&bars->p_full[t]); else mbar_arrive(&bars->p_full[t]);
-      }
+      if (lane == 0) mbar_arrive(&bars->p_full[t]);
       // off the critical path (P is handed over): this tile's block log-sum-exps
       if (BLSE && ADASPA_BLSE_ABL != 1) blse_store(tsum[0], tsum[1], half0[0], half0[1], ntile);
       ++ntile;
@@ -1134,7 +1351,7 @@ static cudaError_t launch_one(const CUtensorMap& tq, const CUtensorMap& tk, cons
   if (e != cudaSuccess) return e;
   const int grid = p.num_items < num_sms ? p.num_items : num_sms;
   if (grid <= 0) return cudaSuccess;
-  kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, p);
+  kern<<<grid, threads_of<D>(), smem, st>>>(tq, tk, tv, p);
   return cudaGetLastError();
 }
 
