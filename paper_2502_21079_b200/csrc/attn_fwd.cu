@@ -67,11 +67,15 @@ constexpr int kThreads = 640;  // d=64: 4 + 16 softmax warps (16 rows per warp)
 #ifndef ADASPA_ROW_THREAD
 #define ADASPA_ROW_THREAD 1
 #endif
-// d=128: one S row per softmax thread (4 + 8 warps), see the kRowThread softmax below
-template <int D>
-constexpr bool row_thread() { return D == 128 && ADASPA_ROW_THREAD != 0; }
-template <int D>
-constexpr int threads_of() { return row_thread<D>() ? 384 : kThreads; }
+// One S row per softmax thread (4 + 8 warps, the kRowThread softmax below) everywhere except the
+// dense d=64 pass: A/B on one box (profiles/r02v_*, r02w_*): d=128 K1 / K4 unchanged, the fused search
+// pass -4% (its block sums need no shuffles); d=64 K4 +1.5% and fused search -4%, but dense d=64 K1
+// 795 -> 715 TFLOP/s (MUFU-bound: two MUFU-issuing warps per SMSP instead of four).  ADASPA_ROW_THREAD=0
+// builds the 16-row softmax everywhere (A/B).
+template <int D, int MODE>
+constexpr bool row_thread() { return ADASPA_ROW_THREAD != 0 && !(D == 64 && MODE == kModeDense); }
+template <int D, int MODE>
+constexpr int threads_of() { return row_thread<D, MODE>() ? 384 : kThreads; }
 __device__ __forceinline__ uint32_t s_col(int t) { return static_cast<uint32_t>(t) * 128u; }
 __device__ __forceinline__ uint32_t o_col(int t) { return 256u + static_cast<uint32_t>(t) * 128u; }
 // d=64: O_t uses 64 of its 128 columns, so P_t gets the other 64 instead of aliasing S_t.  The next
@@ -191,7 +195,7 @@ static_assert(Smem<128>::kBytes <= 232448 && Smem<64>::kBytes <= 232448, "over 2
 // log-sum-exp is written for the fused block-mass reduction), kSparse (K4: the merged CSR stream).
 // QTWO: a q tile is two 64-row q-blocks (sparse B=64); KVTWO: a kv tile is two 64-row kv blocks.
 template <int D, bool QTWO, bool KVTWO, int MODE>
-__global__ void __launch_bounds__(threads_of<D>(), 1)
+__global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, const AttnParams p) {
   constexpr bool SPARSE = MODE == kModeSparse;
@@ -200,7 +204,7 @@ __global__ void __launch_bounds__(threads_of<D>(), 1)
   // skip the exponentials of fully masked 64-column halves: only where they are common (the B=64
   // pairs of the sparse stream); elsewhere the branch costs registers for nothing
   constexpr bool kSkipDead = SPARSE && KVTWO;
-  constexpr bool kRowThread = row_thread<D>();
+  constexpr bool kRowThread = row_thread<D, MODE>();
   constexpr int kSoftWarps = kRowThread ? 4 : 8;  // softmax warps per q tile
   using S = Smem<D>;
   constexpr int NS = S::kNS;
@@ -581,7 +585,7 @@ __global__ void __launch_bounds__(threads_of<D>(), 1)
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t s_addr = tmem + lane_base + s_col(t);
     const uint32_t o_addr = tmem + lane_base + o_col(t);
-    const uint32_t p_addr = tmem + lane_base + p_col<D>(t);  // d=128: P over S columns [0, 64)
+    const uint32_t p_addr = tmem + lane_base + p_col<D>(t);  // d=128: P over S columns [0, 64); d=64: O's spare 64
     const float sl2 = p.scale_log2;
     uint32_t sph = 0, oph = 0;
     int icnt = 0;
@@ -591,6 +595,8 @@ __global__ void __launch_bounds__(threads_of<D>(), 1)
     int ntile = 0;
     float* blse_row = nullptr;  // BLSE: this row of the block-LSE scratch (per item)
     bool blse_ok = false;
+    uint32_t rt_pfph = 0;  // kSepP (d=64): p_free phase; the n-th normal tile (n >= 1) waits for PV n-1
+    int rt_pcnt = 0;
     for (;;) {
       mbar_wait(&bars->s_full[t], sph);
       sph ^= 1;
@@ -675,6 +681,11 @@ __global__ void __launch_bounds__(threads_of<D>(), 1)
       reg_fence32(s + 32);
       reg_fence32(s + 64);
       reg_fence32(s + 96);
+      if (kSepP) {  // S_t is in registers: the next QK_t may overwrite it
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->s_loaded[t]);
+      }
       // dead halves (kSkipDead: masked for every row of the warp) skip their exponentials and stay
       // out of the max; a partial block (or an unneeded half without kSkipDead) is masked to -inf
       const bool deadA = kSkipDead && limA == 0, deadB = kSkipDead && limB <= 64;
@@ -698,6 +709,14 @@ __global__ void __launch_bounds__(threads_of<D>(), 1)
       }
       const float mxa = deadA ? -INFINITY : fmaxf(mx0, mx1), mxb = deadB ? -INFINITY : fmaxf(mx2, mx3);
       const float mx = fmaxf(mxa, mxb) * sl2;
+      if (kSepP) {  // PV of the previous tile has read P_t and accumulated into O_t
+        if (rt_pcnt > 0) {
+          mbar_wait(&bars->p_free[t], rt_pfph);
+          rt_pfph ^= 1;
+          tc_fence_after();
+        }
+        ++rt_pcnt;
+      }
       float alpha = 1.0f;
       bool rescale = false;
       if (mx > m_used + kRescaleThreshold) {  // also true when m_used == -inf (and mx finite)
@@ -1351,7 +1370,7 @@ static cudaError_t launch_one(const CUtensorMap& tq, const CUtensorMap& tk, cons
   if (e != cudaSuccess) return e;
   const int grid = p.num_items < num_sms ? p.num_items : num_sms;
   if (grid <= 0) return cudaSuccess;
-  kern<<<grid, threads_of<D>(), smem, st>>>(tq, tk, tv, p);
+  kern<<<grid, threads_of<D, MODE>(), smem, st>>>(tq, tk, tv, p);
   return cudaGetLastError();
 }
 
