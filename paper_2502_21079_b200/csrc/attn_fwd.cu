@@ -597,9 +597,12 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
     bool blse_ok = false;
     uint32_t rt_pfph = 0;  // kSepP (d=64): p_free phase; the n-th normal tile (n >= 1) waits for PV n-1
     int rt_pcnt = 0;
+    int tr_k = 0;
+    (void)tr_k;
     for (;;) {
       mbar_wait(&bars->s_full[t], sph);
       sph ^= 1;
+      ADASPA_TRACE_EV(0);
       tc_fence_after();
       const TileInfo& inf = bars->info[t][icnt & 1];
       ++icnt;
@@ -681,6 +684,7 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
       reg_fence32(s + 32);
       reg_fence32(s + 64);
       reg_fence32(s + 96);
+      ADASPA_TRACE_EV(1);
       if (kSepP) {  // S_t is in registers: the next QK_t may overwrite it
         tc_fence_before();
         __syncwarp();
@@ -738,6 +742,7 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
         }
       }
       const float mb = (m_used == -INFINITY) ? 0.0f : m_used;
+      ADASPA_TRACE_EV(2);
       // P = 2^(S*scale*log2e - m): FFMA2 for the argument, MUFU.EX2, packed to bf16 pairs: S columns
       // 2j, 2j+1 -> P column j (the TS MMA's A layout)
       const float2 sl2v = make_float2(sl2, sl2);
@@ -781,6 +786,7 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
+      ADASPA_TRACE_EV(3);
       if (lane == 0) mbar_arrive(&bars->p_full[t]);
       if (BLSE && blse_ok) {
         // this tile's per-block log-sum-exps relative to the row's first max (thread-local sums):
