@@ -97,6 +97,9 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define ADASPA_ABLATE 0  // diagnostic builds only: 4 = no softmax (MMA / TMA pipeline alone)
 #endif
 constexpr int kExpPolyMod = ADASPA_EXP_POLY_MOD;
+#ifndef ADASPA_SPEC_MAX
+#define ADASPA_SPEC_MAX 1
+#endif
 #ifndef ADASPA_BLSE_ABL
 #define ADASPA_BLSE_ABL 0  // diagnostic builds only: 1 = no per-tile block-LSE epilogue, 2 = no store
 #endif
@@ -206,6 +209,9 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
   constexpr bool kSkipDead = SPARSE && KVTWO;
   constexpr bool kRowThread = row_thread<D, MODE>();
   constexpr int kSoftWarps = kRowThread ? 4 : 8;  // softmax warps per q tile
+  // speculative first-half exponentials: A/B profiles/r02z_ab_*: K1 +1.8%, fused search -1.9%, K4 +1.3%
+  // at B=128; K4 at B=64 (dead halves) -2.4% and d=64 spills, so not there
+  constexpr bool kSpecMax = ADASPA_SPEC_MAX != 0 && D == 128 && !(SPARSE && KVTWO);
   using S = Smem<D>;
   constexpr int NS = S::kNS;
   constexpr bool kSepP = D == 64;
@@ -700,19 +706,52 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
           s[i] = i < lim ? s[i] : __float_as_uint(-INFINITY);
         }
       }
-      float mx0 = fmaxf(__uint_as_float(s[0]), __uint_as_float(s[1]));
-      float mx1 = fmaxf(__uint_as_float(s[2]), __uint_as_float(s[3]));
-      float mx2 = fmaxf(__uint_as_float(s[64]), __uint_as_float(s[65]));
-      float mx3 = fmaxf(__uint_as_float(s[66]), __uint_as_float(s[67]));
+      const float2 sl2v = make_float2(sl2, sl2);
+      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      // P = 2^(S*scale*log2e - m) for one 64-column half: FFMA2 for the argument, MUFU.EX2, packed to
+      // bf16 pairs (S columns 2j, 2j+1 -> P column j, the TS MMA's A layout); sums into acc
+      auto exp_half = [&](int c, float mbase, uint32_t* pk) {
+        const float2 nm = make_float2(-mbase, -mbase);
 #pragma unroll
-      for (int i = 4; i < 64; i += 4) {
-        mx0 = fmax3(mx0, __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
-        mx1 = fmax3(mx1, __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
-        mx2 = fmax3(mx2, __uint_as_float(s[64 + i]), __uint_as_float(s[65 + i]));
-        mx3 = fmax3(mx3, __uint_as_float(s[66 + i]), __uint_as_float(s[67 + i]));
+        for (int k = 0; k < 32; ++k) {
+          const int i = 64 * c + 2 * k;
+          const float2 x = ffma2(make_float2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sl2v, nm);
+          float2 e;
+          e.x = ex2_approx(x.x);
+          e.y = ex2_approx(x.y);
+          acc[k & 3] = fadd2(acc[k & 3], e);
+          pk[k] = pack_bf16x2(e.x, e.y);
+        }
+      };
+      uint32_t pk[32];
+      // kSpecMax: once the row has a running max, the first half's exponentials go first with it and
+      // the full row max is taken only if that was not safe -- the half's sum above 2^8 (then some
+      // P may exceed 2^8) or the second half's max passing m + 8 (checked before anything is handed
+      // over, so both halves always share one m); otherwise the max waits in the MUFU's shadow
+      bool spec = false;
+      if (kSpecMax && __all_sync(0xffffffffu, m_used > -INFINITY)) {
+        float h0 = fmaxf(__uint_as_float(s[64]), __uint_as_float(s[65]));
+        float h1 = fmaxf(__uint_as_float(s[66]), __uint_as_float(s[67]));
+#pragma unroll
+        for (int i = 4; i < 64; i += 4) {
+          h0 = fmax3(h0, __uint_as_float(s[64 + i]), __uint_as_float(s[65 + i]));
+          h1 = fmax3(h1, __uint_as_float(s[66 + i]), __uint_as_float(s[67 + i]));
+        }
+        const float mh1 = deadB ? -INFINITY : fmaxf(h0, h1) * sl2;
+        if (deadA) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) pk[i] = 0u;
+        } else {
+          exp_half(0, m_used, pk);
+        }
+        const float2 a = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+        const bool ok = (a.x + a.y <= 256.0f) && !(mh1 > m_used + kRescaleThreshold);
+        spec = __all_sync(0xffffffffu, ok);
+        if (!spec) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[i] = make_float2(0.f, 0.f);
+        }
       }
-      const float mxa = deadA ? -INFINITY : fmaxf(mx0, mx1), mxb = deadB ? -INFINITY : fmaxf(mx2, mx3);
-      const float mx = fmaxf(mxa, mxb) * sl2;
       if (kSepP) {  // PV of the previous tile has read P_t and accumulated into O_t
         if (rt_pcnt > 0) {
           mbar_wait(&bars->p_free[t], rt_pfph);
@@ -721,65 +760,69 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
         }
         ++rt_pcnt;
       }
-      float alpha = 1.0f;
-      bool rescale = false;
-      if (mx > m_used + kRescaleThreshold) {  // also true when m_used == -inf (and mx finite)
-        alpha = (m_used == -INFINITY) ? 0.0f : exp2f(m_used - mx);
-        l_sum *= alpha;
-        if (BLSE && m_used == -INFINITY) ref = mx;
-        m_used = mx;
-        rescale = alpha != 0.0f && ntile > 0;
-      }
-      if (__any_sync(0xffffffffu, rescale)) {  // rare: some row's max grew by more than 2^8
-#pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(o_addr + c * 32, r);
-          tmem_ld_wait32(r);
+      if (!spec) {
+        float mx0 = fmaxf(__uint_as_float(s[0]), __uint_as_float(s[1]));
+        float mx1 = fmaxf(__uint_as_float(s[2]), __uint_as_float(s[3]));
+        float mx2 = fmaxf(__uint_as_float(s[64]), __uint_as_float(s[65]));
+        float mx3 = fmaxf(__uint_as_float(s[66]), __uint_as_float(s[67]));
 #pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-          tmem_st32(o_addr + c * 32, r);
+        for (int i = 4; i < 64; i += 4) {
+          mx0 = fmax3(mx0, __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
+          mx1 = fmax3(mx1, __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
+          mx2 = fmax3(mx2, __uint_as_float(s[64 + i]), __uint_as_float(s[65 + i]));
+          mx3 = fmax3(mx3, __uint_as_float(s[66 + i]), __uint_as_float(s[67 + i]));
+        }
+        const float mxa = deadA ? -INFINITY : fmaxf(mx0, mx1), mxb = deadB ? -INFINITY : fmaxf(mx2, mx3);
+        const float mx = fmaxf(mxa, mxb) * sl2;
+        float alpha = 1.0f;
+        bool rescale = false;
+        if (mx > m_used + kRescaleThreshold) {  // also true when m_used == -inf (and mx finite)
+          alpha = (m_used == -INFINITY) ? 0.0f : exp2f(m_used - mx);
+          l_sum *= alpha;
+          if (BLSE && m_used == -INFINITY) ref = mx;
+          m_used = mx;
+          rescale = alpha != 0.0f && ntile > 0;
+        }
+        if (__any_sync(0xffffffffu, rescale)) {  // rare: some row's max grew by more than 2^8
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(o_addr + c * 32, r);
+            tmem_ld_wait32(r);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            tmem_st32(o_addr + c * 32, r);
+          }
+        }
+        if (deadA) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) pk[i] = 0u;
+        } else {
+          exp_half(0, (m_used == -INFINITY) ? 0.0f : m_used, pk);
         }
       }
       const float mb = (m_used == -INFINITY) ? 0.0f : m_used;
       ADASPA_TRACE_EV(2);
-      // P = 2^(S*scale*log2e - m): FFMA2 for the argument, MUFU.EX2, packed to bf16 pairs: S columns
-      // 2j, 2j+1 -> P column j (the TS MMA's A layout)
-      const float2 sl2v = make_float2(sl2, sl2);
-      const float2 nm = make_float2(-mb, -mb);
-      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      float half0 = 0.0f;  // the row sum over columns 0-63 (BLSE with KVTWO: kv block id0)
+      // first half of P stored: the MMA thread may start PV on kv rows 0-63
+      tmem_st32(p_addr, pk);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->p_half[t]);
+      float half0;  // the row sum over columns 0-63 (BLSE with KVTWO: kv block id0)
+      {
+        const float2 h01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+        half0 = h01.x + h01.y;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t pk[32];
-        const bool dead = c == 0 ? deadA : deadB;
-        if (dead) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) pk[i] = 0u;
-        } else {
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const int i = 64 * c + 2 * k;
-            const float2 x = ffma2(make_float2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sl2v, nm);
-            float2 e;
-            e.x = ex2_approx(x.x);
-            e.y = ex2_approx(x.y);
-            acc[k & 3] = fadd2(acc[k & 3], e);
-            pk[k] = pack_bf16x2(e.x, e.y);
-          }
-        }
-        tmem_st32(p_addr + c * 32, pk);
-        if (c == 0) {  // first half of P stored: the MMA thread may start PV on kv rows 0-63
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bars->p_half[t]);
-          const float2 h01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-          half0 = h01.x + h01.y;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) acc[i] = make_float2(0.f, 0.f);
-        }
+        for (int i = 0; i < 4; ++i) acc[i] = make_float2(0.f, 0.f);
       }
+      if (deadB) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pk[i] = 0u;
+      } else {
+        exp_half(1, mb, pk);
+      }
+      tmem_st32(p_addr + 32, pk);
       const float2 h23 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
       const float half1 = h23.x + h23.y;
       l_sum += half0 + half1;
