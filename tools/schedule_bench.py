@@ -15,7 +15,8 @@ sweep: the kernel-level analogue of the scaling study (sparsit
     720p at 5/8/16/24 s (latent frames f = 4 s + 1 at 16 fps, 45 x 80 patches, 256 text tokens),
     blocks 64 and 128.  Per-mode times are measured (3 timed runs each after one warm-up) and the
     50-step schedule time is composed from them: 9 full + 1 full+search + sparse + cached-search
-    steps.  Reports K1 / K4 TFLOP/s, kept density and the schedule speedup over all-dense.
+    steps (t_w: the fused dense pass + K3).  Reports K1 / K4 TFLOP/s, kept density and the schedule
+    speedup over all-dense.
 """
 import argparse
 import json
@@ -114,6 +115,15 @@ def run_sweep(args):
             ws = torch.empty(ada.sparse_workspace_bytes(desc), dtype=torch.uint8, device="cuda")
             t_full = time_call(lambda: ada.dense_attn_lse(q, k, v, o=o, lse=lse, **kw))
             t_search = time_call(lambda: ada.lse_cached_search(q, k, lse, block_mass=M, **kw))
+            # the search step t_w: the fused dense pass (block LSEs + masses, in head passes whose
+            # scratch stays under 32 GB) then K3 (SPARSITY mode has no fused selection epilogue)
+            per_head = ada.fused_search_workspace_bytes(desc, 1)
+            hpp = max(1, min(H, (32 << 30) // per_head))
+            fws = torch.empty(ada.fused_search_workspace_bytes(desc, hpp), dtype=torch.uint8, device="cuda")
+            Mf = torch.empty_like(M)
+            t_fused = time_call(lambda: ada.dense_attn_lse_search(q, k, v, o=o, lse=lse, block_mass=Mf, workspace=fws,
+                                                                  **kw))
+            del fws, Mf
             t_sel = time_call(lambda: ada.select_blocks(M, heads_desc=desc, mode=ada.SELECT_SPARSITY,
                                                         target=[0.9] * H, out=out))
             t_sparse = time_call(lambda: ada.block_sparse_attn(q, k, v, out.row_ptr, out.col_idx, o=o,
@@ -121,12 +131,13 @@ def run_sweep(args):
             fl, nnz = kept_flops(lay, out, d)
             dense_fl = 4.0 * N * N * d * H
             modes = S.trace(50, 10, [10, 30])
-            sched = sum({S.FULL: t_full, S.FULL_SEARCH: t_full + t_search + t_sel, S.SPARSE: t_sparse,
+            sched = sum({S.FULL: t_full, S.FULL_SEARCH: t_fused + t_sel, S.SPARSE: t_sparse,
                          S.CACHED_SEARCH_SPARSE: t_search + t_sel + t_sparse}[m] for m in modes)
             rec = {"video_s": secs, "latent_frames": f, "seq_len": N, "block": block, "nb": nb,
                    "selection": "sparsity 0.9 per head (row-wise top-k + text sink)",
                    "K1_ms": round(t_full, 2), "K1_tflops": round(dense_fl / t_full / 1e9, 1),
-                   "K2_ms": round(t_search, 2), "K3_ms": round(t_sel, 3),
+                   "K2_ms": round(t_search, 2), "K3_ms": round(t_sel, 3), "fused_search_ms": round(t_fused, 2),
+                   "fused_heads_per_pass": hpp,
                    "K4_ms": round(t_sparse, 2), "K4_tflops_kept": round(fl / t_sparse / 1e9, 1),
                    "kept_density": round(nnz / (H * nb * nb), 4),
                    "schedule_ms_per_layer": round(sched, 1), "all_dense_ms_per_layer": round(50 * t_full, 1),
