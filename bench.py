@@ -562,7 +562,11 @@ def run_ours(args):
         del qh, kh, vh, oh
 
     peaks, src = load_peaks()
+    # ncu DRAM bytes per launch were captured on the HYV-110K step (profiles/ncu_traffic.json top
+    # level); other configs report them only if captured for that config (a sub-dict by name)
     traffic = load_traffic()
+    if args.config != "hyv110k":
+        traffic = traffic.get(args.config, {}) if isinstance(traffic.get(args.config), dict) else {}
     launches = (hp.kernels_per_run() + 2 + 4) * K   # + K1 alone, K2 (cached LSE) and K3 (4) per step
     variants = None
     if ws == 1 and not args.no_variants and args.config == "hyv110k":

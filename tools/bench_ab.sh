@@ -1,4 +1,4 @@
-for r in 1 2; do
+for r in 1 2 3; do
 for lib in lib_rt0 lib_cur; do
 ADASPA_LIB=variants/$lib.so python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-variants > gpurun_out/r02ab_$lib.$r.json 2>/dev/null
 python -c "
