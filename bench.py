@@ -355,6 +355,27 @@ def variant_tiers(hp, q, k, v, lay, peaks, reps=5):
             "head_nnz": [int(x) for x in csr.head_nnz[0].tolist()]}
 
 
+def variant_schedule_and_sweep(args):
+    """BASELINE configs[4] (one HYV-110K layer through the 50-step schedule, T_s = {10, 30}, drifting
+    inputs) and the length sweep of SURVEY.md f2 (HunyuanVideo 720p 5-24 s,
+    block 128, sparsity 0.9), from tools/schedule_bench.py, so the driver's run
+    measures them too."""
+    import argparse as _ap
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_schedule_bench", os.path.join(ROOT, "tools", "schedule_bench.py"))
+    sb = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(sb)
+    ns = _ap.Namespace(key_steps=["10,30"], recall=args.recall)
+    sched = sb.run_schedule(ns, emit=False)[0]
+    sweep = sb.run_sweep(ns, blocks=(128,), seconds=(5, 8, 16, 24), emit=False)
+    torch.cuda.empty_cache()
+    return {"schedule_hyv110k_50steps": sched,
+            "length_sweep_block128": [{k: r[k] for k in ("video_s", "seq_len", "nb", "K1_tflops", "K4_tflops_kept",
+                                                         "kept_density", "fused_search_ms", "K1_ms",
+                                                         "schedule_ms_per_layer", "speedup_vs_dense")}
+                                      for r in sweep]}
+
+
 def variant_config(name, args, peaks, traffic, reps=5, sm_mhz=None):
     """Another BASELINE config (CogVideoX-shaped layer, configs[1]) through the whole hot path:
     per-kernel median ms and roofline."""
@@ -575,6 +596,7 @@ def run_ours(args):
         torch.cuda.empty_cache()
         variants["cogx45k_recall0.9"] = variant_config("cogx45k", args, peaks, traffic,
                                                        sm_mhz=(clocks or {}).get("sm_mhz"))
+        variants.update(variant_schedule_and_sweep(args))
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         qc, kc, vc = workloads.generate_qkv(lay, device=dev)

@@ -44,7 +44,7 @@ def drift(base, sigma, gen):
     return out
 
 
-def run_schedule(args):
+def run_schedule(args, emit=True):
     lay = workloads.layout_for("hyv110k")
     dev = "cuda"
     q0, k0, v0 = workloads.generate_qkv(lay, device=dev)
@@ -80,7 +80,8 @@ def run_schedule(args):
                "steps_per_mode": {m: len(v) for m, v in per_mode.items()},
                "attention_ms_per_layer": round(total, 1), "all_dense_ms_per_layer": round(50 * full, 1),
                "speedup_vs_dense": round(50 * full / total, 3), "final_mask_density": round(dens, 4)}
-        print(json.dumps(rec), flush=True)
+        if emit:
+            print(json.dumps(rec), flush=True)
         results.append(rec)
     return results
 
@@ -97,10 +98,10 @@ def time_call(fn, it=3):
     return e0.elapsed_time(e1) / it
 
 
-def run_sweep(args):
+def run_sweep(args, blocks=(64, 128), seconds=(5, 8, 16, 24), emit=True):
     results = []
-    for block in (64, 128):
-        for secs in (5, 8, 16, 24):
+    for block in blocks:
+        for secs in seconds:
             f = 4 * secs + 1
             lay = workloads.layout_for("hyv110k", f=f, block=block)
             t0 = time.time()
@@ -142,7 +143,8 @@ def run_sweep(args):
                    "kept_density": round(nnz / (H * nb * nb), 4),
                    "schedule_ms_per_layer": round(sched, 1), "all_dense_ms_per_layer": round(50 * t_full, 1),
                    "speedup_vs_dense": round(50 * t_full / sched, 3), "gen_s": round(time.time() - t0, 1)}
-            print(json.dumps(rec), flush=True)
+            if emit:
+                print(json.dumps(rec), flush=True)
             results.append(rec)
             del q, k, v, o, lse, M, out, ws
             torch.cuda.empty_cache()
