@@ -1,17 +1,21 @@
-"""Small K1 -> K2 -> K3 -> K4 runs for compute-sanitizer (memcheck / racecheck / synccheck):
-d = 128 at blocks 128 and 64, both text orders, two items per head."""
+"""Small runs of the whole path for compute-sanitizer (memcheck / racecheck / synccheck): HotPath.run
+(K1-free search step: the fused dense pass + block masses with the selection epilogue + CSR, then K4),
+K1 alone and K2 + K3 (the cached search), at d = 128 and 64, blocks 128 and 64, both text orders, two
+items per head -- every softmax layout (row per thread; 16 rows per warp for dense d=64)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import workloads
 from paper_2502_21079_b200.hotpath import HotPath
 
-for tf, block in ((False, 128), (True, 128), (False, 64)):
-    lay = workloads.layout_for("tiny_tf" if tf else "tiny", f=6, h=10, w=11, n_text=77, head_dim=128,
+for d, tf, block in ((128, False, 128), (128, True, 128), (128, False, 64), (64, True, 64), (64, False, 128)):
+    lay = workloads.layout_for("tiny_tf" if tf else "tiny", f=6, h=10, w=11, n_text=77, head_dim=d,
                                block=block, heads=2)
     q, k, v = (x.cuda() for x in workloads.generate_qkv(lay))
     hp = HotPath(1, lay.heads, lay.n, lay.head_dim, lay.block, lay.n_text, lay.text_first, targets=0.9)
     o = hp.run(q, k, v)
+    od = hp.dense(q, k, v, lse=torch.empty_like(hp.lse))
+    hp.select(hp.cached_search(q, k))
     torch.cuda.synchronize()
-    assert torch.isfinite(o.float()).all()
+    assert torch.isfinite(o.float()).all() and torch.isfinite(od.float()).all()
 print("sanitize case ok")
