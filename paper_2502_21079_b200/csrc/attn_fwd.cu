@@ -21,7 +21,7 @@
 //   warps 4-11  softmax for q tile 0, warps 12-19 for q tile 1; each warp owns 16 whole rows
 //               (16-lane TMEM shapes, a thread quad per row: max / sum by quad shuffles, no
 //               exchange between warps).  exp2 domain, conditional rescaling of O (only when the
-//               running max grows by more than 8 in log2 units -- exact, the final normalisation
+//               running max grows by more than kRescaleThreshold in log2 units -- exact, the final normalisation
 //               uses the same max), P written back to TMEM as bf16 over the first 64 columns of S_t.
 #include "attn.cuh"
 #include "common.cuh"
@@ -84,7 +84,15 @@ __device__ __forceinline__ uint32_t o_col(int t) { return 256u + static_cast<uin
 // work).  d=128 has no spare TMEM and keeps P in S (the chain stays).
 template <int D>
 __device__ __forceinline__ uint32_t p_col(int t) { return D == 64 ? o_col(t) + 64u : s_col(t); }
-constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// The running max m moves only when a row's max passes it by more than T (log2 units); P = 2^(x - m)
+// then stays <= 2^T (bf16 and the fp32 sums and O accumulation hold 2^24 x |V| x N with room to
+// spare), and the final normalisation uses the same m, so the result is exact for any T.  Fewer moves
+// mean fewer O rescales (a TMEM read-modify-write of the tile's O): A/B profiles/r02ai_ab*.txt,
+// T = 8 -> 12 -> 24: K4 1018 -> 1052 -> 1070 TFLOP/s, K1 1153 -> 1158 -> 1187 (same box).
+#ifndef ADASPA_RESCALE_LOG2
+#define ADASPA_RESCALE_LOG2 24
+#endif
+constexpr float kRescaleThreshold = static_cast<float>(ADASPA_RESCALE_LOG2);  // log2 units
 // One exp group in ADASPA_EXP_POLY_MOD on an FMA-pipe polynomial instead of MUFU.EX2 (0: none).
 // Round 1 measured 1 in 8 best; after the round-1 softmax changes (16-row warps, vote-gated max) the
 // MUFU is no longer the limit and the polynomial's ~6 instructions per element cost more than they
@@ -595,7 +603,7 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
     const float sl2 = p.scale_log2;
     uint32_t sph = 0, oph = 0;
     int icnt = 0;
-    float m_used = -INFINITY;  // running max (log2 units), moved only when the row max passes it by 8
+    float m_used = -INFINITY;  // running max (log2 units), moved only when the row max passes it by kRescaleThreshold
     float l_sum = 0.0f;
     float ref = 0.0f;          // BLSE: the row's first running max
     int ntile = 0;
@@ -725,8 +733,8 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
       };
       uint32_t pk[32];
       // kSpecMax: once the row has a running max, the first half's exponentials go first with it and
-      // the full row max is taken only if that was not safe -- the half's sum above 2^8 (then some
-      // P may exceed 2^8) or the second half's max passing m + 8 (checked before anything is handed
+      // the full row max is taken only if that was not safe -- the half's sum above 2^T (then some
+      // P may exceed 2^T, T = kRescaleThreshold) or the second half's max passing m + T (checked before anything is handed
       // over, so both halves always share one m); otherwise the max waits in the MUFU's shadow
       bool spec = false;
       if (kSpecMax && __all_sync(0xffffffffu, m_used > -INFINITY)) {
@@ -745,7 +753,7 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
           exp_half(0, m_used, pk);
         }
         const float2 a = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-        const bool ok = (a.x + a.y <= 256.0f) && !(mh1 > m_used + kRescaleThreshold);
+        const bool ok = (a.x + a.y <= exp2f(kRescaleThreshold)) && !(mh1 > m_used + kRescaleThreshold);
         spec = __all_sync(0xffffffffu, ok);
         if (!spec) {
 #pragma unroll
@@ -783,7 +791,7 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
           m_used = mx;
           rescale = alpha != 0.0f && ntile > 0;
         }
-        if (__any_sync(0xffffffffu, rescale)) {  // rare: some row's max grew by more than 2^8
+        if (__any_sync(0xffffffffu, rescale)) {  // rare: some row's max grew by more than 2^T
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
             uint32_t r[32];
@@ -1104,7 +1112,7 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
       bool rescale = false;
       const float m_prev[2] = {m_used[0], m_used[1]};
       const float l_prev[2] = {l_sum[0], l_sum[1]};
-      // m_used moves when the quad's row max exceeds it by more than 2^8 (log2 units)
+      // m_used moves when the quad's row max exceeds it by more than 2^T (log2 units)
       auto update_max = [&](const float lmx0, const float lmx1) {
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
@@ -1156,7 +1164,7 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
       ADASPA_TRACE_EV(2);
       wait_p_free();  // kSepP: PV of the previous tile has read P_t and accumulated into O_t
       ++pcnt;
-      if (__any_sync(0xffffffffu, rescale)) {  // rare: the running max grew by more than 2^8
+      if (__any_sync(0xffffffffu, rescale)) {  // rare: the running max grew by more than 2^T
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
           uint32_t r[16];
