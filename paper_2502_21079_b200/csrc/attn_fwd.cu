@@ -70,7 +70,8 @@ constexpr int kThreads = 640;  // d=64: 4 + 16 softmax warps (16 rows per warp)
 // One S row per softmax thread (4 + 8 warps, the kRowThread softmax below) everywhere except the
 // dense d=64 pass: A/B on one box (profiles/r02v_*, r02w_*): d=128 K1 / K4 unchanged, the fused search
 // pass -4% (its block sums need no shuffles); d=64 K4 +1.5% and fused search -4%, but dense d=64 K1
-// 795 -> 715 TFLOP/s (MUFU-bound: two MUFU-issuing warps per SMSP instead of four).  ADASPA_ROW_THREAD=0
+// 795 -> 715 TFLOP/s (MUFU-bound: two MUFU-issuing warps per SMSP instead of four; still -2.3% with
+// the 2^24 rescale threshold, r02ak).  ADASPA_ROW_THREAD=0
 // builds the 16-row softmax everywhere (A/B).
 template <int D, int MODE>
 constexpr bool row_thread() { return ADASPA_ROW_THREAD != 0 && !(D == 64 && MODE == kModeDense); }
@@ -218,8 +219,9 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
   constexpr bool kRowThread = row_thread<D, MODE>();
   constexpr int kSoftWarps = kRowThread ? 4 : 8;  // softmax warps per q tile
   // speculative first-half exponentials: A/B profiles/r02z_ab_*: K1 +1.8%, fused search -1.9%, K4 +1.3%
-  // at B=128; K4 at B=64 (dead halves) -2.4% and d=64 spills, so not there
-  constexpr bool kSpecMax = ADASPA_SPEC_MAX != 0 && D == 128 && !(SPARSE && KVTWO);
+  // at B=128; K4 at B=64 -2.4% with the rescale threshold at 2^8, +1.2% at 2^24 (r02ak); not at d=64
+  // (its registers spill)
+  constexpr bool kSpecMax = ADASPA_SPEC_MAX != 0 && D == 128;
   using S = Smem<D>;
   constexpr int NS = S::kNS;
   constexpr bool kSepP = D == 64;
