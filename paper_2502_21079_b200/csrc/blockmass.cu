@@ -87,8 +87,9 @@ __global__ void __launch_bounds__(kWarps * 32, 5) block_mass_kernel(BlockMassPar
   if constexpr (KPL > 0) {
     __syncthreads();  // the row is rewritten in place below (non-candidates -> 0, padding to 32*KPL)
     if (warp == 0) {
+      __shared__ selrow::Bracket br;
       selrow::SmemRow<KPL> mr(mrow);
-      selrow::select_row<KPL>(p.sel, static_cast<int>(row), lane, mr, [&](int j) { return mrow[j]; });
+      selrow::select_row<KPL>(p.sel, static_cast<int>(row), lane, mr, br, [&](int j) { return mrow[j]; });
     }
   }
 }

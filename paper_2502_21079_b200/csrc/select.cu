@@ -51,23 +51,28 @@ __global__ void __launch_bounds__(256, KPL <= 32 ? 3 : 1) select_rows_kernel(Sel
   const int lane = threadIdx.x & 31;
   if (warp >= p.rows) return;
   const float* mrow = p.mass + static_cast<int64_t>(warp) * p.grid.nb;
+  __shared__ selrow::Bracket br[8];
   selrow::RegRow<KPL> mr;
-  selrow::select_row<KPL>(p, warp, lane, mr, [&](int j) { return __ldg(mrow + j); });
+  selrow::select_row<KPL>(p, warp, lane, mr, br[threadIdx.x >> 5], [&](int j) { return __ldg(mrow + j); });
 }
 
-// Per batch element: head Recall from the base selection, tiers, new k per (b,h).
-__global__ void select_tiers_kernel(SelectTierParams p) {
+// Per batch element: head Recall from the base selection, tiers, new k per (b,h).  One warp per head
+// sums the head's rows (lane-strided, then a fixed-order shuffle tree: deterministic).
+__global__ void __launch_bounds__(1024) select_tiers_kernel(SelectTierParams p) {
   __shared__ double rec[kMaxHeads];
   const int b = blockIdx.x;
   const int H = p.heads;
-  for (int h = threadIdx.x; h < H; h += blockDim.x) {
-    const int bh = b * H + h;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int h = wid; h < H; h += nw) {
+    const int64_t r0 = static_cast<int64_t>(b * H + h) * p.nb;
     double num = 0.0, den = 0.0;
-    for (int q = 0; q < p.nb; ++q) {
-      num += p.row_kept[(int64_t)bh * p.nb + q];
-      den += p.row_total[(int64_t)bh * p.nb + q];
+    for (int q = lane; q < p.nb; q += 32) {
+      num += p.row_kept[r0 + q];
+      den += p.row_total[r0 + q];
     }
-    rec[h] = den > 0.0 ? num / den : 0.0;
+    num = warp_sum_f64(num);
+    den = warp_sum_f64(den);
+    if (lane == 0) rec[h] = den > 0.0 ? num / den : 0.0;
   }
   __syncthreads();
   int nabove = 0;
@@ -186,11 +191,16 @@ __global__ void __launch_bounds__(1024) select_scan_kernel(SelectFinalParams p) 
   }
 }
 
-// One warp per row: row_ptr, ascending col_idx from the kept bitmask, LPT slot.
+// One warp per row: row_ptr, LPT slot, and the row's ascending col_idx.  Per 32 keep words (1024
+// kv-blocks): lane i loads word i, an exclusive scan of the word counts gives each lane its place in
+// the row, the lane expands its set bits (lowest first) into a per-warp shared-memory run there, and
+// the warp copies the run out with coalesced stores.
 __global__ void __launch_bounds__(256) select_write_kernel(SelectWriteParams p) {
+  __shared__ int stage[8][1024];
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= p.rows) return;
+  int* buf = stage[threadIdx.x >> 5];
   const uint32_t* bits = p.bits + static_cast<int64_t>(row) * p.nwords;
   const int start = p.head_base[row / p.nb] + p.local_off[row];
   if (lane == 0) {
@@ -198,10 +208,26 @@ __global__ void __launch_bounds__(256) select_write_kernel(SelectWriteParams p) 
     if (p.row_order) p.row_order[atomicAdd(p.hist + p.row_nnz[row], 1)] = row;
   }
   int off = start;
-  for (int i = 0; i < p.nwords; ++i) {
-    const uint32_t w = bits[i];
-    if ((w >> lane) & 1u) p.col_idx[off + __popc(w & ((1u << lane) - 1u))] = i * 32 + lane;
-    off += __popc(w);
+  for (int i0 = 0; i0 < p.nwords; i0 += 32) {
+    const int i = i0 + lane;
+    uint32_t w = i < p.nwords ? __ldg(bits + i) : 0u;
+    const int c = __popc(w);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int pos = incl - c;
+    while (w) {
+      buf[pos++] = i * 32 + __ffs(w) - 1;
+      w &= w - 1u;
+    }
+    __syncwarp();
+    for (int k = lane; k < total; k += 32) p.col_idx[off + k] = buf[k];
+    __syncwarp();
+    off += total;
   }
 }
 
@@ -243,7 +269,7 @@ cudaError_t launch_select(const SelectLaunch& L, cudaStream_t st) {
   if (L.tiers) {
     rp.k_per_bh = nullptr;
     if ((e = launch_rows(rp, st)) != cudaSuccess) return e;
-    select_tiers_kernel<<<L.batch, 256, 0, st>>>(L.tier);
+    select_tiers_kernel<<<L.batch, 1024, 0, st>>>(L.tier);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     rp.k_per_bh = L.tier.k_per_bh;
   }

@@ -17,11 +17,15 @@
 // Each bisection round tests one threshold t against every element with FMA-pipe arithmetic only:
 // [m < t] = sat((t - m) * +inf) -- a positive difference (denormals included: no flush to zero)
 // gives +inf -> 1, zero gives NaN -> 0, a negative one -inf -> 0 -- so a round costs a packed
-// subtract, a saturating multiply and a packed FMA per element instead of an integer compare and a
-// select on the (half-rate) ALU pipe (round 1: ALU 81% busy, ~30 rounds per row).  RECALL stops the
-// bisection once the bracket is narrower than 2^-17 relative (kStopBits) and walks to the exact fp64
+// subtract, a saturating multiply and two packed FMA-pipe accumulations (the tail sum and the count)
+// per element pair instead of an integer compare and a select on the (half-rate) ALU pipe.  The
+// count tells how many elements are still inside the bracket: once at most 32 are, the bisection
+// stops (~6 rounds on the paper-shaped masses instead of ~25 to a 64-ulp bracket) and the cut is
+// resolved exactly among those few (per-warp shared-memory slots, (mass desc, id asc) keys, fp64
+// prefix sums).  RECALL checks that resolution in fp64 and, if the fp32 bisection's rounding put the
+// cut outside the bracket (or ties keep more than 32 elements inside it), walks to the exact fp64
 // cut over neighbouring distinct values, so the result is the fp64 definition's whatever the fp32
-// rounding of the bisection; SPARSITY counts are exact (integers below 2^24 in fp32).
+// rounding; SPARSITY counts are exact (integers below 2^24 in fp32).
 #pragma once
 #include "select.cuh"
 
@@ -115,8 +119,51 @@ struct SmemRow {
   }
 };
 
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+  const uint32_t h = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(v >> 32));
+  const uint32_t l = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(v >> 32) == h ? static_cast<uint32_t>(v) : 0u);
+  return (static_cast<uint64_t>(h) << 32) | l;
+}
+
+// The few candidates left inside the bisection bracket, one slot per lane (per-warp shared memory):
+// key = mass bits << 32 | ~id orders them like the selection does -- (mass desc, id asc) is key desc.
+struct Bracket {
+  uint64_t key[32];
+  double val[32];
+};
+
+// Writes the candidates with bit pattern in [lo, hi) (lo = 0: every candidate below hi, zero masses
+// included, non-candidates told apart by id) into br in (i, lane) order; returns their number (<= 32
+// whenever the caller's count of the bracket is).
+template <int KPL, bool kSumAbove, class Row>
+__device__ __forceinline__ int collect_bracket(const Row& mr, int lane, uint32_t lo, uint32_t hi, int nb, int f0,
+                                               int f1, Bracket& br, double& above) {
+  int n = 0;
+  double g = 0.0;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int j = i * 32 + lane;
+    const float m = mr.get(i, lane);
+    const uint32_t b = __float_as_uint(m);
+    if (kSumAbove) g += f2d_volatile(b >= hi ? m : 0.0f);  // fp64 mass at or above the bracket
+    const bool in = b >= lo && b < hi && (lo > 0u || (j < nb && !(j >= f0 && j < f1)));
+    const uint32_t bal = __ballot_sync(0xffffffffu, in);
+    const int slot = n + __popc(bal & ((1u << lane) - 1u));
+    if (in && slot < 32) {
+      br.key[slot] = (static_cast<uint64_t>(b) << 32) | static_cast<uint32_t>(~j);
+      br.val[slot] = f2d_volatile(m);
+    }
+    n += __popc(bal);
+  }
+  if (kSumAbove) above = warp_sum_f64(g);
+  __syncwarp();
+  return n < 32 ? n : 32;
+}
+
 // Selects row `row` (= (b*H + h)*nb + qb) of the masses that load(j) returns (j < nb) and writes
-// its kept bitmask (p.bits), count (p.row_nnz), kept and total mass (p.row_kept, p.row_total).
+// its kept bitmask (p.bits, unless null), count (p.row_nnz), kept and total mass (p.row_kept,
+// p.row_total); returns the count.  kWords (KPL <= 32): lane i also returns keep word i (kv-blocks
+// 32i..32i+31) in *lane_word.
 // Called by a whole warp (all 32 lanes, warp-uniform row).  `mr` holds the candidate masses from the
 // first pass on (RegRow or SmemRow; a SmemRow may alias the storage load() reads: element (i, lane)
 // is read before it is written, by the same thread).
@@ -125,8 +172,9 @@ struct SmemRow {
 // [t0, t1), so candidate-ness is recomputed from the id where it matters instead of being stored.
 // Non-candidates hold mass 0 in `mr`; a candidate of mass 0 only matters when the cut is at 0
 // (SPARSITY with k above the number of positive masses), which takes a separate path.
-template <int KPL, class Row, class Load>
-__device__ __forceinline__ void select_row(const SelectRowsParams& p, int row, int lane, Row& mr, Load load) {
+template <int KPL, bool kWords = false, class Row, class Load>
+__device__ __forceinline__ int select_row(const SelectRowsParams& p, int row, int lane, Row& mr, Bracket& br,
+                                          Load load, uint32_t* lane_word = nullptr) {
   const int nb = p.grid.nb;
   const int bh = row / nb;
   const int qb = row - bh * nb;
@@ -139,20 +187,20 @@ __device__ __forceinline__ void select_row(const SelectRowsParams& p, int row, i
   constexpr int KP = (KPL + 1) / 2;
   auto mval = [&](int i) -> float { return mr.get(i, lane); };
   auto is_forced = [&](int j) -> bool { return j >= f0 && j < f1; };
-  double ssum = 0.0, fsum = 0.0;  // candidate mass, forced mass
+  double tsum = 0.0, fsum = 0.0;  // row mass, forced mass
+  const unsigned nforced = static_cast<unsigned>(f1 - f0);
+  // the forced (text) blocks first: a SmemRow aliasing load()'s storage zeroes them below
+  for (int j = f0 + lane; j < f1; j += 32) fsum += f2d_volatile(load(j));
 #pragma unroll
   for (int i = 0; i < 2 * KP; ++i) {
     const int j = i * 32 + lane;
     const bool valid = i < KPL && j < nb;
     const float x = valid ? load(j) : 0.0f;
-    const bool forced = is_forced(j);
-    const double xd = f2d_volatile(x);
-    if (forced) fsum += xd; else ssum += xd;
-    mr.set(i, lane, forced ? 0.0f : x);  // candidate masses only (forced mass is F)
+    tsum += f2d_volatile(x);
+    mr.set(i, lane, static_cast<unsigned>(j - f0) < nforced ? 0.0f : x);  // candidate masses only
   }
-  const double S = warp_sum_f64(ssum);  // sum of the candidate masses
+  const double T = warp_sum_f64(tsum);
   const double F = warp_sum_f64(fsum);
-  const double T = S + F;
 
   // decision: 0 = keep all, 1 = forced only (+top-1 if none forced), 2 = cut at v*
   int decision;
@@ -166,7 +214,7 @@ __device__ __forceinline__ void select_row(const SelectRowsParams& p, int row, i
     R = __dmul_rn(r, T);
     if (r >= 1.0) decision = 0;
     else if (F >= R || r <= 0.0) decision = 1;
-    else if (F + S < R) decision = 0;  // rounding made the full candidate set fall short: keep everything
+    else if (T < R) decision = 0;  // rounding made the full row fall short: keep everything
     else decision = 2;
   } else {                   // SPARSITY
     kk = p.k_per_bh ? p.k_per_bh[bh] : p.k_head[h];
@@ -184,77 +232,128 @@ __device__ __forceinline__ void select_row(const SelectRowsParams& p, int row, i
   };
 
   uint32_t vstar = 0;
-  int ties_take = 0;
+  int ties_take = 0, ties_all = 0;  // ties at the cut taken / present (all taken: no tie ranks needed)
+  bool kept_known = false;          // kept_mass already known from the exact resolution (RECALL)
+  double kept_mass = 0.0;
   if (decision == 2) {
     float mx = 0.0f;
 #pragma unroll
     for (int i = 0; i < KPL; ++i) mx = fmaxf(mx, mval(i));
     const uint32_t bmax = warp_max_u32(__float_as_uint(mx));
+    // Bracket [lo, hi) of bit patterns holding the cut.  Every round also counts the slots below its
+    // threshold (all 64*KP slots, zeros of non-candidates included), so the number of slots inside
+    // the bracket is known; once it is at most 32 the bisection stops and the cut is resolved
+    // exactly among those few candidates (resolve_bracket below).  Measured on HYV-110K / CogX-45K
+    // masses: ~6 rounds instead of ~25 (DESIGN.md §6 K3).
+    uint32_t lo = 0u, hi = bmax + 1u;
+    float nlo = 0.0f, nhi = static_cast<float>(64 * KP);  // slots below lo / below hi
+    bool resolved = false;
     if (p.mode == 0) {
-      // RECALL: v* = the largest candidate value v with F + sum_{cand, m >= v} m >= R (fp64).  F + S >= R
+      // RECALL: v* = the largest candidate value v with F + sum_{cand, m >= v} m >= R (fp64).  T >= R
       // here, so v* is a positive mass (zeros add nothing).  Predicate on the TAIL: sum_{m < t} m <=
-      // budget = F + S - R.  The tail is small next to the kept mass, so fp32 resolves it at the scale
-      // of the masses near the cut.  Invariant: tail(lo) <= budget < tail(hi).
-      const float budget = static_cast<float>((F + S) - R);
-      uint32_t lo = 0u, hi = bmax + 1u;
-      while (hi - lo > kStopBits) {
-        const uint32_t mid = lo + ((hi - lo) >> 1);
+      // budget = T - R.  The tail is small next to the kept mass, so fp32 resolves it at the scale
+      // of the masses near the cut.  Invariant: tail(lo) <= budget < tail(hi) (in fp32; the exact
+      // resolution checks it in fp64 and falls back to the walk when rounding broke it).
+      const float budget = static_cast<float>(T - R);
+      // first probe: every candidate below budget / ncand sums to less than the budget, so that
+      // threshold is almost always a valid lo and skips the rounds spent on the lower exponents
+      uint32_t probe = __float_as_uint(budget * (0.999f / static_cast<float>(ncand)));
+      while (hi - lo > kStopBits && nhi - nlo > 32.0f) {
+        uint32_t mid = lo + ((hi - lo) >> 1);
+        if (probe > lo && probe < hi) mid = probe;
+        probe = 0u;
         const float tf = __uint_as_float(mid);
         const float2 t2 = make_float2(tf, tf);
         float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+        float2 c0 = make_float2(0.f, 0.f), c1 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int q = 0; q < KP; ++q) {
           const float2 mq = mr.get2(q, lane);
           const float2 d = sub2(t2, mq);
           const float2 s = make_float2(pos_step(d.x), pos_step(d.y));
-          if (q & 1) a1 = fma2(s, mq, a1); else a0 = fma2(s, mq, a0);
+          if (q & 1) { a1 = fma2(s, mq, a1); c1 = add2(c1, s); } else { a0 = fma2(s, mq, a0); c0 = add2(c0, s); }
         }
-        const float2 a = add2(a0, a1);
-        if (warp_sum_f32(a.x + a.y) <= budget) lo = mid; else hi = mid;
+        const float2 a = add2(a0, a1), c = add2(c0, c1);
+        const float tail = warp_sum_f32(a.x + a.y);
+        const float cnt = warp_sum_f32(c.x + c.y);
+        if (tail <= budget) { lo = mid; nlo = cnt; } else { hi = mid; nhi = cnt; }
       }
-      // snap to a positive value present in the row (the sum only changes at present values), then walk
-      const uint32_t lo1 = lo > 0u ? lo : 1u;
-      uint32_t v = 0xFFFFFFFFu;
-#pragma unroll
-      for (int i = 0; i < KPL; ++i) {
-        const uint32_t b = __float_as_uint(mval(i));
-        v = b >= lo1 && b < v ? b : v;
-      }
-      v = warp_min_u32(v);
-      if (F + sum_ge(v) >= R) {
-        for (;;) {  // up while the next larger present value still reaches R
-          uint32_t u = 0xFFFFFFFFu;
-#pragma unroll
-          for (int i = 0; i < KPL; ++i) {
-            const uint32_t b = __float_as_uint(mval(i));
-            u = b > v && b < u ? b : u;
+      if (nhi - nlo <= 32.0f) {
+        // G = F + the candidate mass at or above hi (fp64); the bracket's candidates in (mass desc,
+        // id asc) order extend it one by one: v* is the first whose prefix reaches R
+        double above = 0.0;
+        const int n = collect_bracket<KPL, true>(mr, lane, lo > 0u ? lo : 1u, hi, nb, f0, f1, br, above);
+        const double G = F + above;
+        if (G >= R) lo = hi;  // fp32 put the cut below hi, fp64 says at or above: walk up from hi
+        if (G < R && n > 0) {
+          uint64_t key = 0;
+          double pre = 0.0;
+          if (lane < n) {
+            key = br.key[lane];
+            for (int s = 0; s < n; ++s) pre += br.key[s] >= key ? br.val[s] : 0.0;  // precede-or-equal
           }
-          u = warp_min_u32(u);
-          if (u == 0xFFFFFFFFu || F + sum_ge(u) < R) break;
-          v = u;
-        }
-      } else {
-        for (;;) {  // down to the next smaller positive present value until R is reached
-          uint32_t u = 0u;
-#pragma unroll
-          for (int i = 0; i < KPL; ++i) {
-            const uint32_t b = __float_as_uint(mval(i));
-            u = b < v && b > u ? b : u;
+          const bool reached = lane < n && G + pre >= R;
+          if (__any_sync(0xffffffffu, reached)) {
+            const uint64_t first = warp_max_u64(reached ? key : 0ull);  // the earliest reached in order
+            vstar = static_cast<uint32_t>(first >> 32);
+            const bool tie = lane < n && static_cast<uint32_t>(key >> 32) == vstar;
+            ties_take = __popc(__ballot_sync(0xffffffffu, tie && key >= first));
+            ties_all = __popc(__ballot_sync(0xffffffffu, tie));
+            // the kept mass is the prefix that reached R: G + pre of the first reached candidate
+            const int fl = __ffs(__ballot_sync(0xffffffffu, lane < n && key == first)) - 1;
+            kept_mass = G + __shfl_sync(0xffffffffu, pre, fl);
+            kept_known = true;
+            resolved = true;
           }
-          u = warp_max_u32(u);
-          if (u == 0u) break;  // cannot happen (F + S >= R): v stays the smallest positive value
-          v = u;
-          if (F + sum_ge(v) >= R) break;
         }
       }
-      vstar = v;
+      if (!resolved) {
+        // walk: snap to a positive value present in the row (the sum only changes at present
+        // values), then step to the exact fp64 cut over neighbouring distinct values
+        const uint32_t lo1 = lo > 0u ? lo : 1u;
+        uint32_t v = 0xFFFFFFFFu;
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) {
+          const uint32_t b = __float_as_uint(mval(i));
+          v = b >= lo1 && b < v ? b : v;
+        }
+        v = warp_min_u32(v);
+        if (F + sum_ge(v) >= R) {
+          for (;;) {  // up while the next larger present value still reaches R
+            uint32_t u = 0xFFFFFFFFu;
+#pragma unroll
+            for (int i = 0; i < KPL; ++i) {
+              const uint32_t b = __float_as_uint(mval(i));
+              u = b > v && b < u ? b : u;
+            }
+            u = warp_min_u32(u);
+            if (u == 0xFFFFFFFFu || F + sum_ge(u) < R) break;
+            v = u;
+          }
+        } else {
+          for (;;) {  // down to the next smaller positive present value until R is reached
+            uint32_t u = 0u;
+#pragma unroll
+            for (int i = 0; i < KPL; ++i) {
+              const uint32_t b = __float_as_uint(mval(i));
+              u = b < v && b > u ? b : u;
+            }
+            u = warp_max_u32(u);
+            if (u == 0u) break;  // cannot happen (T >= R): v stays the smallest positive value
+            v = u;
+            if (F + sum_ge(v) >= R) break;
+          }
+        }
+        vstar = v;
+      }
     } else {
       // SPARSITY: the largest v with at least k candidates >= v.  Invariant: count(>= lo) >= k >
       // count(>= hi); count(>= t) = #{m > pred(t)}, pred(t) the float just below t (t >= 1 here, so
-      // the zeros of non-candidates never count; lo = 0 counts every candidate).
-      uint32_t lo = 0u, hi = bmax + 1u;
+      // the zeros of non-candidates never count; lo = 0 counts every candidate).  Counts are exact
+      // (integers below 2^24 in fp32), so the bracket always holds the cut.
       const float kf = static_cast<float>(kk);
-      while (hi - lo > 1u) {
+      float clo = static_cast<float>(ncand), chi = 0.0f;  // candidates >= lo / >= hi
+      while (hi - lo > 1u && clo - chi > 32.0f) {
         const uint32_t mid = lo + ((hi - lo) >> 1);
         const float pf = __uint_as_float(mid - 1u);
         const float2 p2 = make_float2(pf, pf);
@@ -266,39 +365,63 @@ __device__ __forceinline__ void select_row(const SelectRowsParams& p, int row, i
           if (q & 1) c1 = add2(c1, s); else c0 = add2(c0, s);
         }
         const float2 c = add2(c0, c1);
-        if (warp_sum_f32(c.x + c.y) >= kf) lo = mid; else hi = mid;
+        const float cnt = warp_sum_f32(c.x + c.y);
+        if (cnt >= kf) { lo = mid; clo = cnt; } else { hi = mid; chi = cnt; }
       }
-      vstar = lo;
+      if (clo - chi <= 32.0f) {
+        // the (k - count(>= hi))-th candidate of the bracket in (mass desc, id asc) order is the last kept
+        double unused = 0.0;
+        const int n = collect_bracket<KPL, false>(mr, lane, lo, hi, nb, f0, f1, br, unused);
+        const int need = kk - static_cast<int>(chi);  // 1 <= need <= n
+        uint64_t key = 0;
+        int rank = -1;
+        if (lane < n) {
+          key = br.key[lane];
+          rank = 0;
+          for (int s = 0; s < n; ++s) rank += br.key[s] > key ? 1 : 0;
+        }
+        const uint64_t last = warp_max_u64(rank == need - 1 ? key : 0ull);
+        vstar = static_cast<uint32_t>(last >> 32);
+        const bool tie = lane < n && static_cast<uint32_t>(key >> 32) == vstar;
+        ties_take = __popc(__ballot_sync(0xffffffffu, tie && key >= last));
+        ties_all = __popc(__ballot_sync(0xffffffffu, tie));
+        resolved = true;
+      } else {
+        vstar = lo;
+      }
     }
-    // mass / count strictly above the cut, ties at the cut (candidates only; at a cut of 0 the ties
-    // are the zero-mass candidates, told from non-candidates by id)
-    double sgt = 0.0;
-    int cgt = 0, ctie = 0;
+    if (!resolved) {
+      // mass / count strictly above the cut, ties at the cut (candidates only; at a cut of 0 the ties
+      // are the zero-mass candidates, told from non-candidates by id)
+      double sgt = 0.0;
+      int cgt = 0, ctie = 0;
 #pragma unroll
-    for (int i = 0; i < KPL; ++i) {
-      const int j = i * 32 + lane;
-      const uint32_t b = __float_as_uint(mval(i));
-      if (b > vstar) {
-        sgt += f2d_volatile(mval(i));
-        ++cgt;
-      } else if (b == vstar && (vstar > 0u || (j < nb && !is_forced(j)))) {
-        ++ctie;
+      for (int i = 0; i < KPL; ++i) {
+        const int j = i * 32 + lane;
+        const uint32_t b = __float_as_uint(mval(i));
+        if (b > vstar) {
+          sgt += f2d_volatile(mval(i));
+          ++cgt;
+        } else if (b == vstar && (vstar > 0u || (j < nb && !is_forced(j)))) {
+          ++ctie;
+        }
       }
-    }
-    sgt = warp_sum_f64(sgt);
-    cgt = warp_sum_i32(cgt);
-    ctie = warp_sum_i32(ctie);
-    if (p.mode == 0) {
-      double acc = F + sgt;
-      const double vv = (double)__uint_as_float(vstar);
-      ties_take = 0;
-      while (acc < R && ties_take < ctie) {
-        acc += vv;
-        ++ties_take;
+      sgt = warp_sum_f64(sgt);
+      cgt = warp_sum_i32(cgt);
+      ctie = warp_sum_i32(ctie);
+      ties_all = ctie;
+      if (p.mode == 0) {
+        double acc = F + sgt;
+        const double vv = (double)__uint_as_float(vstar);
+        ties_take = 0;
+        while (acc < R && ties_take < ctie) {
+          acc += vv;
+          ++ties_take;
+        }
+        if (ties_take == 0) ties_take = 1;  // v* itself belongs to the minimal prefix
+      } else {
+        ties_take = kk - cgt;
       }
-      if (ties_take == 0) ties_take = 1;  // v* itself belongs to the minimal prefix
-    } else {
-      ties_take = kk - cgt;
     }
   }
 
@@ -328,42 +451,64 @@ __device__ __forceinline__ void select_row(const SelectRowsParams& p, int row, i
     top1 = bj;
   }
 
-  // keep flags -> bitmask words (word i = ballot over kv-blocks 32i..32i+31)
-  uint32_t* bits_out = p.bits + static_cast<int64_t>(row) * p.nwords;
+  // keep flags -> bitmask words (word i = ballot over kv-blocks 32i..32i+31); with kWords, lane i also
+  // returns word i in lane_word (KPL <= 32: the caller writes the CSR row from the words)
+  uint32_t* bits_out = p.bits ? p.bits + static_cast<int64_t>(row) * p.nwords : nullptr;
   double kept = 0.0;
   int nnz = 0;
-  int tie_seen = 0;
-#pragma unroll
-  for (int i = 0; i < KPL; ++i) {
-    const int j = i * 32 + lane;
-    const bool valid = j < nb;
-    const bool forced = valid && is_forced(j);
-    const uint32_t b = __float_as_uint(mval(i));
-    bool keep;
-    if (decision == 0) {
-      keep = valid;
-    } else if (decision == 1) {
-      keep = forced || j == top1;
-    } else {
-      const bool tie = b == vstar && valid && !forced;
-      const uint32_t tb = __ballot_sync(0xffffffffu, tie);
-      const int rank = tie_seen + __popc(tb & ((1u << lane) - 1u));
-      tie_seen += __popc(tb);
-      keep = forced || b > vstar || (tie && rank < ties_take);
-    }
-    const uint32_t word = __ballot_sync(0xffffffffu, keep);
+  uint32_t lw = 0;
+  auto emit = [&](int i, uint32_t word) {
     if (i * 32 < nb) {
-      if (lane == 0) bits_out[i] = word;
+      if (bits_out && lane == 0) bits_out[i] = word;
       nnz += __popc(word);
     }
-    if (keep && !forced) kept += f2d_volatile(mval(i));  // forced blocks are always kept (mass F)
+    if (kWords && lane == i) lw = word;
+  };
+  if (decision == 2 && vstar > 0u && ties_take >= ties_all) {
+    // every candidate at or above the cut is kept (no tie is split): keep = forced or m >= v*
+    // (non-candidates hold 0 < v*)
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int j = i * 32 + lane;
+      const bool forced = static_cast<unsigned>(j - f0) < static_cast<unsigned>(f1 - f0) && j < nb;
+      const bool cand_keep = __float_as_uint(mval(i)) >= vstar;
+      emit(i, __ballot_sync(0xffffffffu, forced || cand_keep));
+      if (!kept_known) kept += f2d_volatile(cand_keep ? mval(i) : 0.0f);
+    }
+    if (!kept_known) kept = warp_sum_f64(kept) + F;
+    else kept = kept_mass;
+  } else {
+    int tie_seen = 0;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int j = i * 32 + lane;
+      const bool valid = j < nb;
+      const bool forced = valid && is_forced(j);
+      const uint32_t b = __float_as_uint(mval(i));
+      bool keep;
+      if (decision == 0) {
+        keep = valid;
+      } else if (decision == 1) {
+        keep = forced || j == top1;
+      } else {
+        const bool tie = b == vstar && valid && !forced;
+        const uint32_t tb = __ballot_sync(0xffffffffu, tie);
+        const int rank = tie_seen + __popc(tb & ((1u << lane) - 1u));
+        tie_seen += __popc(tb);
+        keep = forced || b > vstar || (tie && rank < ties_take);
+      }
+      emit(i, __ballot_sync(0xffffffffu, keep));
+      if (keep && !forced) kept += f2d_volatile(mval(i));  // forced blocks are always kept (mass F)
+    }
+    kept = warp_sum_f64(kept) + F;
   }
-  kept = warp_sum_f64(kept) + F;
   if (lane == 0) {
     p.row_nnz[row] = nnz;
     p.row_kept[row] = kept;
     p.row_total[row] = T;
   }
+  if (kWords) *lane_word = lw;
+  return nnz;
 }
 
 }  // namespace selrow

@@ -169,6 +169,36 @@ def test_select_blocks_exact_large_nb(ada, nv, nt, mode):
             assert got == exp, f"nb={nb} {mode} h{h} row {p}: {len(got)} kept vs {len(exp)} (first {got[:6]} / {exp[:6]})"
 
 
+@pytest.mark.parametrize("levels", [3, 24, 400])
+@pytest.mark.parametrize("mode", ["recall", "sparsity"])
+def test_select_blocks_heavy_ties(ada, mode, levels):
+    """K3 when many candidates share the cut value: masses drawn from `levels` distinct values, so the
+    bisection's bracket can end with more than 32 equal masses (the exact-walk / tie-count fallback
+    of select_row) or with a handful (the in-bracket resolution).  Ties are taken in ascending id
+    order (the (mass desc, id asc) greedy, PAPER.md:436-448 / reading R10); bit-exact against the
+    oracle on identical masses, both modes, with and without the text sink."""
+    H, nv, nt, B = 4, 40000, 150, 64
+    blocks = oracle.block_map(nv, nt, B, False)
+    nb = len(blocks)
+    g = torch.Generator().manual_seed(5 + levels)
+    vals = torch.rand(levels, generator=g, dtype=torch.float64) * 3.0 + 0.01
+    Mt = vals[torch.randint(0, levels, (1, H, nb, nb), generator=g)].float()
+    q = torch.empty(1, H, nv + nt, 64, dtype=torch.bfloat16, device="cuda")
+    desc = ada.make_desc(q, B, nt, False)
+    targets = [0.3, 0.7, 0.9, 0.97]
+    kmode = ada.SELECT_RECALL if mode == "recall" else ada.SELECT_SPARSITY
+    for sink in (True, False):
+        out = ada.select_blocks(Mt.cuda(), heads_desc=desc, mode=kmode, target=targets, flags=int(sink))
+        torch.cuda.synchronize()
+        keep, _, nnz, _ = oracle.select_blocks(Mt[0].double().numpy(), blocks, mode, targets, text_sink=sink)
+        rows = csr_rows(out.row_ptr, out.col_idx)
+        for h in range(H):
+            for p in range(nb):
+                exp = np.nonzero(keep[h, p])[0].tolist()
+                assert rows[h * nb + p] == exp, f"{mode} L{levels} sink{sink} h{h} row {p}: {rows[h * nb + p][:8]} vs {exp[:8]}"
+        np.testing.assert_array_equal(out.head_nnz[0].cpu().numpy(), nnz)
+
+
 @pytest.mark.parametrize("mode", ["recall", "sparsity"])
 def test_select_blocks_zero_masses(ada, mode):
     """K3 on rows where most candidate masses are exactly 0 (fp32 underflow of far blocks in sharp
