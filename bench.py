@@ -289,7 +289,9 @@ def kernel_entries(lay, nb, nnz, kfl, med, peaks, traffic, p90=None, heads=None,
     out = {
         "K1_dense_attn_lse": roofline_entry("tensor", dense_fl / (med["K1"] / 1e3) / 1e12, tens_peak, "TFLOP/s",
                                             traffic.get("K1"), ms=rnd(med["K1"]), ms_p90=rnd(p90.get("K1")),
-                                            exp_frac=round(N * N * H / (med["K1"] / 1e3) / 1e12 / exp_peak, 4)),
+                                            exp_frac=round(N * N * H / (med["K1"] / 1e3) / 1e12 / exp_peak, 4),
+                                            exp_frac_at_clock=round(N * N * H / (med["K1"] / 1e3) / 1e12 /
+                                                                    (16.0 * 148 * (sm_mhz or sm_max) * 1e6 / 1e12), 4)),
     }
     if med.get("FS"):
         # algorithmic work of the fused search = the dense pass's 4N^2dH: the block masses reuse its
@@ -313,8 +315,15 @@ def kernel_entries(lay, nb, nnz, kfl, med, peaks, traffic, p90=None, heads=None,
                                                            "FMA-pipe exponentials too")
     out["K3_select_blocks"] = roofline_entry("hbm", k3_bytes / (med["K3"] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s",
                                              traffic.get("K3"), ms=rnd(med["K3"], 4), ms_p90=rnd(p90.get("K3"), 4))
+    # one exponential per kept (q, k) pair, 4d FLOPs each: at d = 64 the MUFU.EX2 rate (16/clk/SM) bounds
+    # the kept-block rate below the tensor peak -- 4 * 64 * 16 * 148 * clock = 1190 TFLOP/s at 1965 MHz,
+    # 982 at 1620 -- so the entry also reports the exponential rate against MUFU at the run's clock
+    k4_exp = kfl / (4.0 * d) / (med["K4"] / 1e3) / 1e12
     out["K4_block_sparse_attn"] = roofline_entry("tensor", kfl / (med["K4"] / 1e3) / 1e12, tens_peak, "TFLOP/s",
-                                                 traffic.get("K4"), ms=rnd(med["K4"]), ms_p90=rnd(p90.get("K4")))
+                                                 traffic.get("K4"), ms=rnd(med["K4"]), ms_p90=rnd(p90.get("K4")),
+                                                 exp_frac=round(k4_exp / exp_peak, 4),
+                                                 exp_frac_at_clock=round(k4_exp / mufu_clk, 4),
+                                                 mufu_bound_tflops_at_clock=round(4.0 * d * mufu_clk, 1))
     return out
 
 
