@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(1024) select_tiers_kernel(SelectTierParams p) 
   for (int h = wid; h < H; h += nw) {
     const int64_t r0 = static_cast<int64_t>(b * H + h) * p.nb;
     double num = 0.0, den = 0.0;
+#pragma unroll 8
     for (int q = lane; q < p.nb; q += 32) {
       num += p.row_kept[r0 + q];
       den += p.row_total[r0 + q];
@@ -91,9 +92,9 @@ __global__ void __launch_bounds__(1024) select_tiers_kernel(SelectTierParams p) 
 
 // Per (b,h) CTA: exclusive scan of the head's row counts (local offsets), head nnz / Recall
 // (fixed-order fp64 sums: deterministic), and the histogram of row counts for the LPT order.
-__global__ void __launch_bounds__(256) select_head_kernel(SelectFinalParams p) {
-  __shared__ int wsum[8];
-  __shared__ double wk[8], wt[8];
+__global__ void __launch_bounds__(1024) select_head_kernel(SelectFinalParams p) {
+  __shared__ int wsum[32];
+  __shared__ double wk[32], wt[32];
   __shared__ int carry;
   const int bh = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(256) select_head_kernel(SelectFinalParams p) {
   if (tid == 0) carry = 0;
   __syncthreads();
   double kept = 0.0, tot = 0.0;
-  for (int base = 0; base < p.nb; base += 256) {
+  for (int base = 0; base < p.nb; base += 1024) {
     const int q = base + tid;
     const int v = q < p.nb ? p.row_nnz[r0 + q] : 0;
     if (q < p.nb) {
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(256) select_head_kernel(SelectFinalParams p) {
     __syncthreads();
     if (tid == 0) {
       int t = 0;
-      for (int w = 0; w < 8; ++w) t += wsum[w];
+      for (int w = 0; w < 32; ++w) t += wsum[w];
       carry += t;
     }
     __syncthreads();
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(256) select_head_kernel(SelectFinalParams p) {
   __syncthreads();
   if (tid == 0) {
     double k = 0.0, t = 0.0;
-    for (int w = 0; w < 8; ++w) {
+    for (int w = 0; w < 32; ++w) {
       k += wk[w];
       t += wt[w];
     }
@@ -252,7 +253,7 @@ cudaError_t launch_select_final(const SelectLaunch& L, cudaStream_t st) {
   cudaError_t e;
   if (L.fin.row_order && (e = cudaMemsetAsync(L.fin.hist, 0, sizeof(int) * (L.fin.nb + 1), st)) != cudaSuccess)
     return e;
-  select_head_kernel<<<L.fin.bh, 256, 0, st>>>(L.fin);
+  select_head_kernel<<<L.fin.bh, 1024, 0, st>>>(L.fin);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   select_scan_kernel<<<1, 1024, 0, st>>>(L.fin);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
