@@ -16,7 +16,8 @@ $N -k regex:attn_fwd_kernel -c 1 -o gpurun_out/${tag}_k1 -f python tools/prof_st
 $N -k regex:attn_fwd_kernel --launch-skip 2 -c 1 -o gpurun_out/${tag}_k4 -f python tools/prof_step.py hyv110k 1 >> gpurun_out/${tag}_ncu.log 2>&1
 $N -k regex:attn_fwd_kernel --launch-skip 1 -c 1 -o gpurun_out/${tag}_fs -f python tools/prof_step.py hyv110k 1 2 >> gpurun_out/${tag}_ncu.log 2>&1
 $N -k regex:"block_mass|search_kernel|select_rows" -c 3 -o gpurun_out/${tag}_other -f python tools/prof_step.py hyv110k 1 >> gpurun_out/${tag}_ncu.log 2>&1
-for r in k1 k4 fs other; do
+$N -k regex:"select_(rows|head|scan|write)" -c 4 -o gpurun_out/${tag}_k3 -f python tools/k3_bench.py hyv110k 1 >> gpurun_out/${tag}_ncu.log 2>&1
+for r in k1 k4 fs other k3; do
   ncu -i gpurun_out/${tag}_${r}.ncu-rep --page raw --csv > gpurun_out/${tag}_${r}.raw.csv 2>/dev/null
 done
 ncu -i gpurun_out/${tag}_k1.ncu-rep --page source --csv --print-source sass > gpurun_out/${tag}_k1.source.csv 2>/dev/null
