@@ -28,25 +28,36 @@
 
 namespace adaspa {
 
+#ifndef ADASPA_K4_PF
+#define ADASPA_K4_PF 0  // diagnostic: -DADASPA_K4_PF=n prefetches K/V n stream entries ahead into L2 (A/B r02aq: no gain)
+#endif
+
 #ifdef ADASPA_TRACE
 // Diagnostic build only (-DADASPA_TRACE): per-tile clock64 stamps of CTA 0 -- softmax warp 4
 // (q tile 0, column half 0) events 0..3 and the MMA issuer's events -- read back through
 // adaspa_debug_trace().  The product library is built without it.
 __device__ unsigned long long g_trace[4][4096];
 __device__ int g_trace_n[2];
+#ifndef ADASPA_TRACE_SKIP
+#define ADASPA_TRACE_SKIP 0  // tiles skipped before the 1000 recorded ones (-DADASPA_TRACE_SKIP=n: mid-kernel)
+#endif
+#define ADASPA_TRACE_IN(i) ((i) >= ADASPA_TRACE_SKIP && (i) < ADASPA_TRACE_SKIP + 1000)
 #define ADASPA_TRACE_EV(k)                                                                    \
   do {                                                                                        \
-    if (blockIdx.x == 0 && warp == 4 && lane == 0 && tr_k < 1000) g_trace[0][tr_k * 4 + (k)] = clock64(); \
+    if (blockIdx.x == 0 && warp == 4 && lane == 0 && ADASPA_TRACE_IN(tr_k))                   \
+      g_trace[0][(tr_k - ADASPA_TRACE_SKIP) * 4 + (k)] = clock64();                           \
     if ((k) == 3) ++tr_k;                                                                     \
   } while (0)
 #define ADASPA_TRACE_MMA(k)                                                                   \
   do {                                                                                        \
-    if (blockIdx.x == 0 && tr_n < 1000) g_trace[1 + ((k) >> 2)][tr_n * 4 + ((k) & 3)] = clock64(); \
+    if (blockIdx.x == 0 && ADASPA_TRACE_IN(tr_n))                                             \
+      g_trace[1 + ((k) >> 2)][(tr_n - ADASPA_TRACE_SKIP) * 4 + ((k) & 3)] = clock64();        \
     if ((k) == 5) ++tr_n;                                                                     \
   } while (0)
 #define ADASPA_TRACE_TMA(k)                                                                   \
   do {                                                                                        \
-    if (blockIdx.x == 0 && tp_n < 1000) g_trace[3][tp_n * 4 + (k)] = clock64();               \
+    if (blockIdx.x == 0 && ADASPA_TRACE_IN(tp_n))                                             \
+      g_trace[3][(tp_n - ADASPA_TRACE_SKIP) * 4 + (k)] = clock64();                           \
     if ((k) == 3) ++tp_n;                                                                     \
   } while (0)
 #else
@@ -216,6 +227,7 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
   // skip the exponentials of fully masked 64-column halves: only where they are common (the B=64
   // pairs of the sparse stream); elsewhere the branch costs registers for nothing
   constexpr bool kSkipDead = SPARSE && KVTWO;
+  constexpr int kK4Prefetch = ADASPA_K4_PF;  // K4: stream entries between an L2 prefetch and its load
   constexpr bool kRowThread = row_thread<D, MODE>();
   constexpr int kSoftWarps = kRowThread ? 4 : 8;  // softmax warps per q tile
   // speculative first-half exponentials: A/B profiles/r02z_ab_*: K1 +1.8%, fused search -1.9%, K4 +1.3%
@@ -341,6 +353,23 @@ __global__ void __launch_bounds__(threads_of<D, MODE>(), 1)
             s1 = s0 + 64;
             l1 = 0;
             mask = dense_mask;
+          }
+          // K4: warm L2 with the K/V tiles of the entry kK4Prefetch ahead (the gathered tiles of a
+          // head's stream miss L2 now and then; the ring itself holds only 2.5 entries at d=128)
+          if constexpr (SPARSE && kK4Prefetch > 0) {
+            if (e + kK4Prefetch < n_ent) {
+              const uint64_t en = __ldg(reinterpret_cast<const unsigned long long*>(ent_ptr) + e + kK4Prefetch);
+              const int ps0 = p.grid.start(entry_id0(en));
+              const int ps1 = KVTWO ? p.grid.start(entry_id1(en)) : 0;
+              for (int c = 0; c < CH; ++c) {
+                tma_prefetch_l2_4d(&tk, c * 64, ps0, it.h, it.b, pol_kv);
+                tma_prefetch_l2_4d(&tv, c * 64, ps0, it.h, it.b, pol_kv);
+                if (KVTWO) {
+                  tma_prefetch_l2_4d(&tk, c * 64, ps1, it.h, it.b, pol_kv);
+                  tma_prefetch_l2_4d(&tv, c * 64, ps1, it.h, it.b, pol_kv);
+                }
+              }
+            }
           }
           // K
           ADASPA_TRACE_TMA(0);

@@ -35,9 +35,13 @@ ld = sm[:, 1] - sm[:, 0]; mx = sm[:, 2] - sm[:, 1]; ex = sm[:, 3] - sm[:, 2]
 wait = sm[1:, 0] - sm[:-1, 3]; period = np.diff(sm[:, 0])
 for nm, x in (("LDTM", ld), ("max+xchg barrier", mx), ("rescale+exp+P store", ex), ("wait for next S", wait), ("period", period)):
     x = x[10:-10] if len(x) > 40 else x
-    print(f"  {nm:22s} median {np.median(x):8.0f}  p10 {np.percentile(x,10):8.0f}  p90 {np.percentile(x,90):8.0f}")
+    print(f"  {nm:22s} median {np.median(x):8.0f}  p10 {np.percentile(x,10):8.0f}  p90 {np.percentile(x,90):8.0f}  mean {np.mean(x):8.0f}")
+print(f"  periods above 2x median: {int((period > 2 * np.median(period)).sum())} of {len(period)}, "
+      f"{(period[period > 2 * np.median(period)].sum()) / period.sum() * 100:.1f}% of the traced time")
 m = int((mm[:, 3] > 0).sum())
 mm = mm[:m]
+if m < 40:
+    sys.exit(0)
 print(f"MMA issuer: {m} entries")
 names = ["p_full0 seen", "QK0 issued", "p_full1 seen", "QK1 issued"]
 for i in range(4):
