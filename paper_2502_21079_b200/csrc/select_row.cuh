@@ -149,15 +149,16 @@ __device__ __forceinline__ int collect_bracket(const Row& mr, int lane, uint32_t
     const bool in = b >= lo && b < hi && (lo > 0u || (j < nb && !(j >= f0 && j < f1)));
     const uint32_t bal = __ballot_sync(0xffffffffu, in);
     const int slot = n + __popc(bal & ((1u << lane) - 1u));
-    if (in && slot < 32) {
-      br.key[slot] = (static_cast<uint64_t>(b) << 32) | static_cast<uint32_t>(~j);
-      br.val[slot] = f2d_volatile(m);
-    }
+    if (in && slot < 32) br.key[slot] = (static_cast<uint64_t>(b) << 32) | static_cast<uint32_t>(~j);
     n += __popc(bal);
   }
   if (kSumAbove) above = warp_sum_f64(g);
+  n = n < 32 ? n : 32;
   __syncwarp();
-  return n < 32 ? n : 32;
+  // one fp32 -> fp64 conversion per slot (lane s converts slot s), not one per element and pass
+  if (lane < n) br.val[lane] = f2d_volatile(__uint_as_float(static_cast<uint32_t>(br.key[lane] >> 32)));
+  __syncwarp();
+  return n;
 }
 
 // Selects row `row` (= (b*H + h)*nb + qb) of the masses that load(j) returns (j < nb) and writes
