@@ -16,6 +16,8 @@
 #include "common.cuh"
 #include "select.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 using namespace adaspa;
 
 namespace {
@@ -172,6 +174,15 @@ SparseWs sparse_ws_layout(const adaspa_attn_desc* d) {
 
 }  // namespace
 
+// An NVTX range around each compute entry of the C ABI (header-only NVTX3: a no-op unless a tool
+// such as nsys or ncu --nvtx is attached), so profiles group the kernels of one call under its name.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 extern "C" {
 
 int32_t adaspa_abi_version(void) { return ADASPA_ABI_VERSION; }
@@ -196,6 +207,7 @@ const char* adaspa_last_error(void) { return g_last_error.c_str(); }
 
 adaspa_status adaspa_dense_attn_lse(const adaspa_attn_desc* desc, const void* q, const void* k, const void* v,
                                     void* o, float* lse, adaspa_stream_t stream) {
+  NvtxRange nvtx_range("adaspa_dense_attn_lse");
   adaspa_status s;
   if ((s = check_desc(desc)) != ADASPA_OK) return s;
   if ((s = check_ptr16(q, "q")) || (s = check_ptr16(k, "k")) || (s = check_ptr16(v, "v")) ||
@@ -294,6 +306,7 @@ adaspa_status fused_search_passes(const adaspa_attn_desc* desc, const void* q, c
 adaspa_status adaspa_dense_attn_lse_search(const adaspa_attn_desc* desc, const void* q, const void* k, const void* v,
                                            void* o, float* lse, float* block_mass, void* workspace,
                                            size_t workspace_bytes, adaspa_stream_t stream) {
+  NvtxRange nvtx_range("adaspa_dense_attn_lse_search");
   adaspa_status s;
   if ((s = check_desc(desc)) != ADASPA_OK) return s;
   if ((s = check_ptr16(q, "q")) || (s = check_ptr16(k, "k")) || (s = check_ptr16(v, "v")) ||
@@ -312,6 +325,7 @@ adaspa_status adaspa_dense_attn_lse_search(const adaspa_attn_desc* desc, const v
 
 adaspa_status adaspa_lse_cached_search(const adaspa_attn_desc* desc, const void* q, const void* k,
                                        const float* lse, float* block_mass, adaspa_stream_t stream) {
+  NvtxRange nvtx_range("adaspa_lse_cached_search");
   adaspa_status s;
   if ((s = check_desc(desc)) != ADASPA_OK) return s;
   if ((s = check_ptr16(q, "q")) || (s = check_ptr16(k, "k"))) return s;
@@ -454,6 +468,7 @@ adaspa_status adaspa_select_blocks(const adaspa_attn_desc* desc, const float* bl
                                    int32_t* col_idx, int64_t col_capacity, int32_t* row_order, float* head_recall,
                                    int64_t* head_nnz, void* workspace, size_t workspace_bytes,
                                    adaspa_stream_t stream) {
+  NvtxRange nvtx_range("adaspa_select_blocks");
   adaspa_status s;
   if ((s = check_desc(desc)) != ADASPA_OK) return s;
   if (!block_mass) return fail(ADASPA_ERR_INVALID_ARG, "block_mass must not be NULL");
@@ -480,6 +495,7 @@ adaspa_status adaspa_search_select(const adaspa_attn_desc* desc, const void* q, 
                                    int32_t* row_ptr, int32_t* col_idx, int64_t col_capacity, int32_t* row_order,
                                    float* head_recall, int64_t* head_nnz, void* workspace, size_t workspace_bytes,
                                    adaspa_stream_t stream) {
+  NvtxRange nvtx_range("adaspa_search_select");
   adaspa_status s;
   if ((s = check_desc(desc)) != ADASPA_OK) return s;
   if ((s = check_ptr16(q, "q")) || (s = check_ptr16(k, "k")) || (s = check_ptr16(v, "v")) ||
@@ -522,6 +538,7 @@ size_t adaspa_sparse_workspace_bytes(const adaspa_attn_desc* desc) {
 adaspa_status adaspa_block_sparse_attn(const adaspa_attn_desc* desc, const void* q, const void* k, const void* v,
                                        const int32_t* row_ptr, const int32_t* col_idx, void* o, float* lse,
                                        void* workspace, size_t workspace_bytes, adaspa_stream_t stream) {
+  NvtxRange nvtx_range("adaspa_block_sparse_attn");
   adaspa_status s;
   if ((s = check_desc(desc)) != ADASPA_OK) return s;
   if ((s = check_ptr16(q, "q")) || (s = check_ptr16(k, "k")) || (s = check_ptr16(v, "v")) ||
