@@ -244,7 +244,7 @@ __device__ __forceinline__ int select_row(const SelectRowsParams& p, int row, in
     // Bracket [lo, hi) of bit patterns holding the cut.  Every round also counts the slots below its
     // threshold (all 64*KP slots, zeros of non-candidates included), so the number of slots inside
     // the bracket is known; once it is at most 32 the bisection stops and the cut is resolved
-    // exactly among those few candidates (resolve_bracket below).  Measured on HYV-110K / CogX-45K
+    // exactly among those few candidates (collect_bracket and the key order below).  On HYV-110K / CogX-45K
     // masses: ~6 rounds instead of ~25 (DESIGN.md §6 K3).
     uint32_t lo = 0u, hi = bmax + 1u;
     float nlo = 0.0f, nhi = static_cast<float>(64 * KP);  // slots below lo / below hi
