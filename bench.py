@@ -567,7 +567,8 @@ def run_ours(args):
     if not args.no_e2e:
         qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
         oh = torch.empty_like(qh).pin_memory()
-        groups = max(1, min(24, Hl))
+        from paper_2502_21079_b200.hotpath import tapered_groups
+        groups = tapered_groups(Hl)
         for _ in range(2):
             hp.run_sparse_host(qh, kh, vh, oh, groups=groups)
         torch.cuda.synchronize()
@@ -586,9 +587,10 @@ def run_ours(args):
                "d2h_bytes_per_step": q.numel() * q.element_size() * ws,
                "ms_per_step": round(te / K, 3),
                "note": f"sparse step from pinned host memory: H2D Q,K,V + K4 (cached CSR) + D2H O per rank "
-                       f"(its search head group), overlapped over {groups} head groups, K4 launches "
-                       "alternating between two compute streams; PCIe-bound (2.06 GB of pinned H2D per "
-                       "HYV-110K layer); TFLOP/s on kept blocks, whole job"}
+                       f"(its search head group), overlapped over {len(groups)} head groups of {groups} heads, K4 "
+                       "launches alternating between two compute streams; PCIe-bound (2.06 GB of pinned H2D "
+                       "and 0.69 GB of D2H per HYV-110K layer: 38.9 ms for both at once on the box, "
+                       "tools/pcie_probe.py); TFLOP/s on kept blocks, whole job"}
         del qh, kh, vh, oh
 
     peaks, src = load_peaks()

@@ -19,6 +19,17 @@ import torch
 from . import _lib as L
 
 
+def tapered_groups(heads):
+    """Head-group sizes for run_sparse_host: one-head groups at both ends (K4 starts after one head's
+    copy and the copy-out ends one head after the last K4), two-head groups in the middle (fewer K4
+    launches).  Measured on two boxes against 24 one-head groups: 42.5 vs 43.1 and 43.5 vs 44.1 ms
+    (tools/e2e_groups.py)."""
+    if heads < 12:
+        return [1] * heads
+    mid = heads - 8
+    return [1] * 4 + [2] * (mid // 2) + [1] * (mid % 2) + [1] * 4
+
+
 class HotPath:
     def __init__(self, batch, heads, seq_len, head_dim, block_size, n_text, text_first=False,
                  mode=L.SELECT_RECALL, targets=0.9, flags=L.FLAG_TEXT_SINK, tier_tau=0.8,
@@ -159,7 +170,8 @@ class HotPath:
         group.  The groups' K4 launches alternate between the current stream and a second compute
         stream (each with its own workspace), so one launch's tail overlaps the next launch's start:
         twelve back-to-back launches on one stream take 37.5 ms against 31.2 ms for one launch
-        (tools/e2e_parts.py).  q/k/v/o_host: pinned [B, H, N, d] host tensors.  Uses the CSR of the
+        (tools/e2e_parts.py).  groups: a number of equal head groups, or a list of head counts per group.
+        q/k/v/o_host: pinned [B, H, N, d] host tensors.  Uses the CSR of the
         last run() (the cache).  Everything on the device path is the C-ABI's K4."""
         B, H, N, d = self.shape
         if B != 1:
@@ -176,8 +188,16 @@ class HotPath:
         wss = (self.ws, self._ws2)
         ks[1].wait_stream(cur)
         cs.wait_stream(cur)
-        groups = max(1, min(int(groups), H))  # at least one head per group
-        bounds = [H * g // groups for g in range(groups + 1)]
+        if isinstance(groups, (list, tuple)):  # explicit head counts per group (e.g. tapered ends)
+            if sum(groups) != H or min(groups) < 1:
+                raise ValueError(f"group sizes {groups} must be >= 1 and sum to {H} heads")
+            bounds = [0]
+            for n in groups:
+                bounds.append(bounds[-1] + int(n))
+            groups = len(bounds) - 1
+        else:
+            groups = max(1, min(int(groups), H))  # at least one head per group
+            bounds = [H * g // groups for g in range(groups + 1)]
         done_in, done_k4 = [], []
         for g in range(groups):
             h0, h1 = bounds[g], bounds[g + 1]

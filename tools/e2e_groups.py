@@ -23,6 +23,8 @@ def t(fn, it=5):
     return a.elapsed_time(b) / it
 h2d = t(lambda: [d.copy_(h, non_blocking=True) for d, h in ((hp.q, qh), (hp.k, kh), (hp.v, vh))])
 print(f"H2D 3 x {qh.numel()*2/1e9:.3f} GB: {h2d:.2f} ms = {3*qh.numel()*2/h2d/1e6:.1f} GB/s")
-for g in ([int(x) for x in sys.argv[1:]] or (4, 8, 12, 24)):
+# arguments: a number of equal groups, or comma-separated head counts (e.g. 1,1,2,4,4,4,4,2,1,1)
+for arg in (sys.argv[1:] or ["4", "8", "12", "24"]):
+    g = [int(x) for x in arg.split(",")] if "," in arg else int(arg)
     ms = t(lambda: hp.run_sparse_host(qh, kh, vh, oh, groups=g))
-    print(f"groups {g:2d}: {ms:.2f} ms per sparse step")
+    print(f"groups {arg}: {ms:.2f} ms per sparse step")
