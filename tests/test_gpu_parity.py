@@ -391,7 +391,7 @@ def test_end_to_end_tiny(ada):
 
 def test_run_sparse_host_matches_device(ada):
     """HotPath.run_sparse_host (H2D per head group, K4 on the cached CSR, D2H) == the device K4."""
-    from paper_2502_21079_b200.hotpath import HotPath
+    from paper_2502_21079_b200.hotpath import HotPath, tapered_groups
     lay = _lay("tiny", dict(heads=5, head_dim=128, block=128, f=5, h=9, w=11, n_text=37))
     q, k, v = _qkv(lay)
     hp = HotPath(1, lay.heads, lay.n, lay.head_dim, lay.block, lay.n_text, lay.text_first, targets=0.9)
@@ -399,6 +399,10 @@ def test_run_sparse_host_matches_device(ada):
     ref = hp.o_sparse.clone()
     qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
     oh = torch.empty_like(qh).pin_memory()
-    hp.run_sparse_host(qh, kh, vh, oh, groups=3)
-    torch.cuda.synchronize()
-    assert torch.equal(oh, ref.cpu())
+    for groups in (3, [1, 2, 1, 1], tapered_groups(lay.heads)):   # equal groups, explicit sizes, the bench's
+        oh.zero_()
+        hp.run_sparse_host(qh, kh, vh, oh, groups=groups)
+        torch.cuda.synchronize()
+        assert torch.equal(oh, ref.cpu()), groups
+    with pytest.raises(ValueError):
+        hp.run_sparse_host(qh, kh, vh, oh, groups=[2, 2])            # sizes must cover every head

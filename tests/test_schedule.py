@@ -79,3 +79,15 @@ def test_schedule_gpu_matches_oracle_pipeline(fused):
                 so, _ = oracle.masked_attention(qq, kk, vv, blocks, [rows[h * nb + p] for p in range(nb)], scale)
                 compare_out(o[0, h], so, what=f"t{t} h{h} sparse")
     assert [m for (_, _, m) in sch.calls] == oracle.schedule_trace(n_steps, t_w, ks)
+
+
+def test_tapered_groups_cover_every_head():
+    """run_sparse_host's head groups (host logic, no GPU): sizes >= 1 covering every head once, one-head
+    groups at both ends once there are enough heads."""
+    from paper_2502_21079_b200.hotpath import tapered_groups
+    for h in range(1, 200):
+        g = tapered_groups(h)
+        assert sum(g) == h and min(g) >= 1
+        if h >= 12:
+            assert g[:4] == [1] * 4 and g[-4:] == [1] * 4 and max(g) == 2
+    assert tapered_groups(24) == [1, 1, 1, 1] + [2] * 8 + [1, 1, 1, 1]
