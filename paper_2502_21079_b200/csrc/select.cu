@@ -46,7 +46,7 @@ __host__ __device__ int k_from_sparsity(double s, int n) {
 }
 
 template <int KPL>
-__global__ void __launch_bounds__(256, KPL <= 32 ? 3 : 1) select_rows_kernel(SelectRowsParams p) {
+__global__ void __launch_bounds__(256, KPL <= 28 ? 4 : (KPL <= 32 ? 3 : 1)) select_rows_kernel(SelectRowsParams p) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= p.rows) return;
