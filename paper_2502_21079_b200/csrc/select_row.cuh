@@ -163,8 +163,7 @@ __device__ __forceinline__ int collect_bracket(const Row& mr, int lane, uint32_t
 
 // Selects row `row` (= (b*H + h)*nb + qb) of the masses that load(j) returns (j < nb) and writes
 // its kept bitmask (p.bits, unless null), count (p.row_nnz), kept and total mass (p.row_kept,
-// p.row_total); returns the count.  kWords (KPL <= 32): lane i also returns keep word i (kv-blocks
-// 32i..32i+31) in *lane_word.
+// p.row_total); returns the count.
 // Called by a whole warp (all 32 lanes, warp-uniform row).  `mr` holds the candidate masses from the
 // first pass on (RegRow or SmemRow; a SmemRow may alias the storage load() reads: element (i, lane)
 // is read before it is written, by the same thread).
@@ -173,9 +172,9 @@ __device__ __forceinline__ int collect_bracket(const Row& mr, int lane, uint32_t
 // [t0, t1), so candidate-ness is recomputed from the id where it matters instead of being stored.
 // Non-candidates hold mass 0 in `mr`; a candidate of mass 0 only matters when the cut is at 0
 // (SPARSITY with k above the number of positive masses), which takes a separate path.
-template <int KPL, bool kWords = false, class Row, class Load>
+template <int KPL, class Row, class Load>
 __device__ __forceinline__ int select_row(const SelectRowsParams& p, int row, int lane, Row& mr, Bracket& br,
-                                          Load load, uint32_t* lane_word = nullptr) {
+                                          Load load) {
   const int nb = p.grid.nb;
   const int bh = row / nb;
   const int qb = row - bh * nb;
@@ -452,18 +451,19 @@ __device__ __forceinline__ int select_row(const SelectRowsParams& p, int row, in
     top1 = bj;
   }
 
-  // keep flags -> bitmask words (word i = ballot over kv-blocks 32i..32i+31); with kWords, lane i also
-  // returns word i in lane_word (KPL <= 32: the caller writes the CSR row from the words)
+  // keep flags -> bitmask words (word i = ballot over kv-blocks 32i..32i+31)
   uint32_t* bits_out = p.bits ? p.bits + static_cast<int64_t>(row) * p.nwords : nullptr;
   double kept = 0.0;
   int nnz = 0;
   uint32_t lw = 0;
+  // KPL <= 32: lane i keeps word i and the row's words go out in one coalesced store at the end
+  constexpr bool kLaneWords = KPL <= 32;
   auto emit = [&](int i, uint32_t word) {
     if (i * 32 < nb) {
-      if (bits_out && lane == 0) bits_out[i] = word;
+      if (!kLaneWords && bits_out && lane == 0) bits_out[i] = word;
       nnz += __popc(word);
     }
-    if (kWords && lane == i) lw = word;
+    if (kLaneWords && lane == i) lw = word;
   };
   if (decision == 2 && vstar > 0u && ties_take >= ties_all) {
     // every candidate at or above the cut is kept (no tie is split): keep = forced or m >= v*
@@ -508,7 +508,7 @@ __device__ __forceinline__ int select_row(const SelectRowsParams& p, int row, in
     p.row_kept[row] = kept;
     p.row_total[row] = T;
   }
-  if (kWords) *lane_word = lw;
+  if (kLaneWords && bits_out && lane < p.nwords) bits_out[lane] = lw;
   return nnz;
 }
 
