@@ -200,6 +200,33 @@ def test_select_blocks_heavy_ties(ada, mode, levels):
 
 
 @pytest.mark.parametrize("mode", ["recall", "sparsity"])
+def test_select_blocks_extreme_masses(ada, mode):
+    """K3 on masses spread log-uniformly over the whole fp32 range (denormals up to 2^100 in one row)
+    and targets close to 0 and 1: the bisection's first probe (budget / ncand), the counted bracket
+    and the exact fp64 resolution at extreme scales.  Bit-exact against the oracle on identical masses."""
+    H, nv, nt, B = 4, 50000, 150, 64
+    blocks = oracle.block_map(nv, nt, B, False)
+    nb = len(blocks)
+    g = torch.Generator().manual_seed(13)
+    e = torch.rand(1, H, nb, nb, generator=g, dtype=torch.float64) * 250.0 - 149.0   # 2^-149 .. 2^101
+    Mt = torch.exp2(e).float()
+    Mt[Mt == 0] = 1e-45
+    q = torch.empty(1, H, nv + nt, 64, dtype=torch.bfloat16, device="cuda")
+    desc = ada.make_desc(q, B, nt, False)
+    targets = [1e-6, 0.5, 0.999999, 0.9] if mode == "recall" else [0.001, 0.5, 0.99, 0.9]
+    kmode = ada.SELECT_RECALL if mode == "recall" else ada.SELECT_SPARSITY
+    out = ada.select_blocks(Mt.cuda(), heads_desc=desc, mode=kmode, target=targets, flags=1)
+    torch.cuda.synchronize()
+    keep, _, nnz, _ = oracle.select_blocks(Mt[0].double().numpy(), blocks, mode, targets, text_sink=True)
+    rows = csr_rows(out.row_ptr, out.col_idx)
+    for h in range(H):
+        for p in range(nb):
+            exp = np.nonzero(keep[h, p])[0].tolist()
+            assert rows[h * nb + p] == exp, f"{mode} h{h} row {p}: {rows[h * nb + p][:8]} vs {exp[:8]}"
+    np.testing.assert_array_equal(out.head_nnz[0].cpu().numpy(), nnz)
+
+
+@pytest.mark.parametrize("mode", ["recall", "sparsity"])
 def test_select_blocks_zero_masses(ada, mode):
     """K3 on rows where most candidate masses are exactly 0 (fp32 underflow of far blocks in sharp
     heads): SPARSITY budgets larger than the non-zero count must take zero-mass blocks in ascending
